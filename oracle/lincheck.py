@@ -1,0 +1,248 @@
+"""Linearizability checkers -- TEST INFRASTRUCTURE ONLY.
+
+Python restatement of the reference's lincheck module
+(proj/src/lincheck.cpp, proj/src/instrumentation.cpp:94-131) used by tests/
+to judge device event logs recorded by the CUDA heap (BH_FLAG_RECORD).
+
+  decode_history       Recorder::op_end/finish (instrumentation.cpp:94-131)
+  replay_in_order      lincheck.cpp:29-49 over MultisetOracle (seq_heap.hpp:61-80)
+  check_td             lincheck.cpp:53-71
+  check_bu             lincheck.cpp:73-86
+  check_exhaustive     lincheck.cpp:88-154
+  check_mutual_exclusion  lincheck.cpp:156-184
+  check_lock_order     lincheck.cpp:193-217
+  check_bu_overlap_windows lincheck.cpp:219-241
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from sortedcontainers import SortedList
+
+INSERT, DELETE = 0, 1
+EV_INV, EV_RES, EV_ACQ, EV_REL = 0, 1, 2, 3
+
+
+@dataclass
+class LockSpan:
+    node: int
+    acquire_ts: int
+    release_ts: int = 0
+
+
+@dataclass
+class OpRecord:
+    """proj/include/batchheap/history.hpp:42-57."""
+    worker: int
+    opid: int
+    op: int
+    keys: List[int]
+    invoke_ts: int = 0
+    respond_ts: int = 0
+    root_acquire_ts: int = 0
+    root_release_ts: int = 0
+    last_acquire_ts: int = 0
+    last_release_ts: int = 0
+    locks: List[LockSpan] = field(default_factory=list)
+
+
+@dataclass
+class CheckResult:
+    passed: bool
+    detail: str = ""
+    witness: Optional[List[OpRecord]] = None
+
+
+def decode_history(events, op_kinds: Sequence[int], op_keys: Sequence[Sequence[int]],
+                   skip: Optional[set] = None) -> List[OpRecord]:
+    """Build OpRecords from device events (fields ts/op/kind/node).
+
+    ``op_keys[i]`` is the insert argument or the delete result of op i.
+    Ops with no events (aborted: capacity errors) or listed in ``skip`` are
+    dropped, as Recorder::op_abort does."""
+    per_op: Dict[int, list] = {}
+    for e in events:
+        per_op.setdefault(int(e["op"]), []).append((int(e["ts"]), int(e["kind"]), int(e["node"])))
+    records = []
+    for opi, evs in per_op.items():
+        if skip and opi in skip:
+            continue
+        evs.sort()
+        rec = OpRecord(worker=opi, opid=opi, op=int(op_kinds[opi]),
+                       keys=sorted(int(x) for x in op_keys[opi]))
+        open_locks: List[LockSpan] = []
+        for ts, kind, node in evs:
+            if kind == EV_INV:
+                rec.invoke_ts = ts
+            elif kind == EV_RES:
+                rec.respond_ts = ts
+            elif kind == EV_ACQ:
+                open_locks.append(LockSpan(node, ts))
+            elif kind == EV_REL:
+                for span in reversed(open_locks):
+                    if span.node == node and span.release_ts == 0:
+                        span.release_ts = ts
+                        rec.locks.append(span)
+                        break
+                else:
+                    raise ValueError(f"op {opi}: release without acquire on node {node}")
+        if any(s.release_ts == 0 for s in open_locks):
+            raise ValueError(f"op {opi}: lock never released")
+        rec.locks.sort(key=lambda s: s.acquire_ts)
+        for span in rec.locks:
+            if span.node == 1 and rec.root_acquire_ts == 0:
+                rec.root_acquire_ts = span.acquire_ts
+                rec.root_release_ts = span.release_ts
+            if span.release_ts > rec.last_release_ts:
+                rec.last_release_ts = span.release_ts
+                rec.last_acquire_ts = span.acquire_ts
+        records.append(rec)
+    records.sort(key=lambda r: r.invoke_ts)
+    return records
+
+
+def validate(history: List[OpRecord]) -> Optional[str]:
+    """History::validate (proj/src/history.cpp:142-168)."""
+    seen = set()
+    for op in history:
+        if not (op.invoke_ts < op.root_acquire_ts <= op.root_release_ts < op.respond_ts):
+            return f"op {op.opid}: event order broken"
+        for s in op.locks:
+            if not (op.invoke_ts < s.acquire_ts < s.release_ts < op.respond_ts):
+                return f"op {op.opid}: lock outside op window"
+            for t in (s.acquire_ts, s.release_ts):
+                if t in seen:
+                    return f"duplicate timestamp {t}"
+                seen.add(t)
+    return None
+
+
+def _describe(op: OpRecord) -> str:
+    return f"{'ins' if op.op == INSERT else 'del'} #{op.opid}"
+
+
+def replay_in_order(ordered: List[OpRecord], k: int) -> CheckResult:
+    state = SortedList()
+    for op in ordered:
+        if op.op == INSERT:
+            state.update(op.keys)
+            continue
+        take = min(k, len(state))
+        expected = [state.pop(0) for _ in range(take)]
+        if expected != list(op.keys):
+            return CheckResult(False, f"{_describe(op)} returned {op.keys[:4]} but the oracle gives "
+                                      f"{expected[:4]}")
+    return CheckResult(True, witness=ordered)
+
+
+def check_td(history: List[OpRecord], k: int) -> CheckResult:
+    ordered = sorted(history, key=lambda o: o.root_release_ts)
+    for a, b in zip(ordered, ordered[1:]):
+        if b.root_acquire_ts < a.root_release_ts:
+            return CheckResult(False, f"root windows overlap between {_describe(a)} and {_describe(b)}")
+    return replay_in_order(ordered, k)
+
+
+def check_bu(history: List[OpRecord], k: int) -> CheckResult:
+    def key(o):
+        return (o.last_release_ts if o.op == INSERT else o.root_release_ts, o.worker)
+    return replay_in_order(sorted(history, key=key), k)
+
+
+def check_exhaustive(history: List[OpRecord], k: int) -> CheckResult:
+    n = len(history)
+    if n > 20:
+        raise ValueError(f"check_exhaustive: history has {n} ops (max 20)")
+    ops = history
+    dead = set()
+    state = SortedList()
+    order: List[int] = []
+
+    def eligible(e, mask):
+        for f in range(n):
+            if f == e or (mask >> f) & 1:
+                continue
+            if ops[f].respond_ts < ops[e].invoke_ts:
+                return False
+        return True
+
+    def dfs(mask):
+        if len(order) == n:
+            return True
+        if mask in dead:
+            return False
+        for e in range(n):
+            if (mask >> e) & 1 or not eligible(e, mask):
+                continue
+            op = ops[e]
+            if op.op == INSERT:
+                state.update(op.keys)
+                order.append(e)
+                if dfs(mask | (1 << e)):
+                    return True
+                order.pop()
+                for key in op.keys:
+                    state.remove(key)
+            else:
+                take = min(k, len(state))
+                if len(op.keys) != take or list(state[:take]) != list(op.keys):
+                    continue
+                for key in op.keys:
+                    state.remove(key)
+                order.append(e)
+                if dfs(mask | (1 << e)):
+                    return True
+                order.pop()
+                state.update(op.keys)
+        dead.add(mask)
+        return False
+
+    if dfs(0):
+        return CheckResult(True, witness=[ops[i] for i in order])
+    return CheckResult(False, "no valid linearization exists")
+
+
+def check_mutual_exclusion(history: List[OpRecord]) -> Tuple[bool, str]:
+    per_node: Dict[int, list] = {}
+    for op in history:
+        for s in op.locks:
+            per_node.setdefault(s.node, []).append((s.acquire_ts, s.release_ts, op))
+    for node, spans in per_node.items():
+        spans.sort(key=lambda t: t[0])
+        for a, b in zip(spans, spans[1:]):
+            if b[0] < a[1]:
+                return False, f"node {node} held concurrently by {_describe(a[2])} and {_describe(b[2])}"
+    return True, ""
+
+
+def _is_ancestor(a: int, d: int) -> bool:
+    while d > a:
+        d //= 2
+    return d == a
+
+
+def check_lock_order(history: List[OpRecord]) -> Tuple[bool, str]:
+    for op in history:
+        locks = op.locks
+        for i in range(len(locks)):
+            for j in range(i + 1, len(locks)):
+                a, b = locks[i], locks[j]
+                overlap = a.acquire_ts < b.release_ts and b.acquire_ts < a.release_ts
+                if overlap and a.node != b.node and _is_ancestor(b.node, a.node):
+                    return False, f"{_describe(op)} acquired node {a.node} before its ancestor {b.node}"
+    return True, ""
+
+
+def check_bu_overlap_windows(history: List[OpRecord]) -> Tuple[bool, str]:
+    for d in history:
+        if d.op != DELETE or not d.keys:
+            continue
+        dmax = d.keys[-1]
+        for i in history:
+            if i.op != INSERT or not i.keys:
+                continue
+            if i.last_acquire_ts <= d.root_release_ts and d.root_acquire_ts <= i.last_release_ts:
+                if i.keys[0] < dmax:
+                    return False, f"overlap lemma violated: {_describe(i)} vs {_describe(d)}"
+    return True, ""

@@ -1,0 +1,758 @@
+// bh_capi.cu -- host side of the C ABI (include/batchheap_b200.h).
+//
+// Owns device memory, streams and staging, validates arguments exactly where
+// the reference throws, and launches the persistent heap kernel.  No compute
+// happens on the host: every heap mutation is a device operation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "bh_device.cuh"
+#include "bh_internal.h"
+
+namespace bh {
+int ops_u32(const HeapView&, const RunView&, uint32_t, cudaStream_t);
+int ops_u64(const HeapView&, const RunView&, uint32_t, cudaStream_t);
+int info_u32(uint32_t, KernelInfo*);
+int info_u64(uint32_t, KernelInfo*);
+int sort_u32(uint32_t, void*, const uint32_t*, uint64_t, cudaStream_t);
+int sort_u64(uint32_t, void*, const uint32_t*, uint64_t, cudaStream_t);
+int merge_u32(uint32_t, const void*, const void*, void*, void*, uint64_t, cudaStream_t);
+int merge_u64(uint32_t, const void*, const void*, void*, void*, uint64_t, cudaStream_t);
+int check_u32(const HeapView&, unsigned long long*, cudaStream_t);
+int check_u64(const HeapView&, unsigned long long*, cudaStream_t);
+int gather_u32(const HeapView&, unsigned long long, void*, cudaStream_t);
+int gather_u64(const HeapView&, unsigned long long, void*, cudaStream_t);
+
+__global__ void plan_kernel(int kind, uint32_t k, unsigned long long n_keys, unsigned long long n_ops,
+                            bh_op* ops) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n_ops;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        bh_op o;
+        o.kind = kind == 0 ? BH_OP_INSERT : BH_OP_DELETE;
+        const unsigned long long at = i * k;
+        o.len = kind == 0 ? (uint32_t)min((unsigned long long)k, n_keys - at) : 0u;
+        o.offset = at;
+        ops[i] = o;
+    }
+}
+}  // namespace bh
+
+using namespace bh;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(BH_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define BH_CUDA(call)                                  \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+bool valid_k(uint32_t k) { return k >= 1 && k <= 2048 && (k & (k - 1)) == 0; }
+
+// Per-call context for the single-op entry points: its own stream, pinned
+// staging and device scratch, so concurrent host callers become concurrent
+// device operations.
+struct OpCtx {
+    cudaStream_t stream = nullptr;
+    unsigned char* h = nullptr;  // pinned
+    unsigned char* d = nullptr;
+    size_t bytes = 0;
+};
+
+// Layout of an OpCtx buffer.
+struct CtxLayout {
+    size_t op = 0, ticket = 16, status = 24, lens = 28, seq = 32, keys = 64, out;
+    explicit CtxLayout(size_t key_bytes) : out(64 + key_bytes) {}
+};
+
+}  // namespace
+
+struct bh_heap {
+    int device = 0;
+    int variant = 0;
+    uint32_t k = 0;
+    uint32_t key_bits = 0;
+    uint32_t key_size = 0;
+    uint32_t max_nodes = 0;
+    uint32_t flags = 0;
+    unsigned long long slot_count = 0;
+    void* d_keys = nullptr;
+    uint32_t* d_states = nullptr;
+    Header* d_hdr = nullptr;
+    void* d_partial = nullptr;
+    unsigned long long* d_counters = nullptr;
+    unsigned long long* d_tickets = nullptr;  // ring of bulk tickets
+    std::atomic<uint32_t> ticket_next{0};
+    cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;
+    KernelInfo kinfo{};
+    int sm_count = 0;
+    uint32_t max_ctas = 0;
+
+    std::mutex bulk_mu;
+    void* d_stage = nullptr;
+    size_t stage_bytes = 0;
+
+    // RECORD
+    std::mutex rec_mu;
+    DevEvent* d_events = nullptr;
+    uint32_t* d_event_counts = nullptr;
+    uint64_t ev_cap_ops = 0;
+    uint32_t ev_per_op = 0;
+    uint64_t last_run_ops = 0;
+
+    std::mutex ctx_mu;
+    std::vector<OpCtx*> free_ctx;
+    std::vector<OpCtx*> all_ctx;
+
+    HeapView view() const {
+        HeapView v;
+        v.keys = d_keys;
+        v.states = d_states;
+        v.hdr = d_hdr;
+        v.partial = d_partial;
+        v.counters = d_counters;
+        v.slot_count = slot_count;
+        v.k = k;
+        v.max_nodes = max_nodes;
+        v.variant = (uint32_t)variant;
+        v.flags = flags;
+        return v;
+    }
+};
+
+namespace {
+
+constexpr uint32_t kTicketRing = 64;
+
+int launch_ops(bh_heap* h, const RunView& rv, uint32_t ctas, cudaStream_t s) {
+    HeapView hv = h->view();
+    int rc = h->key_bits == 32 ? ops_u32(hv, rv, ctas, s) : ops_u64(hv, rv, ctas, s);
+    if (rc != BH_OK) return fail(rc, std::string("heap kernel launch failed: ") +
+                                         cudaGetErrorString(cudaGetLastError()));
+    return BH_OK;
+}
+
+uint32_t pick_ctas(bh_heap* h, uint64_t n_ops, const bh_run_cfg* cfg) {
+    uint64_t c = (cfg && cfg->ctas) ? std::min<uint64_t>(cfg->ctas, h->max_ctas) : h->max_ctas;
+    c = std::min<uint64_t>(c, n_ops);
+    return (uint32_t)std::max<uint64_t>(c, 1);
+}
+
+// Events per op sized from the tree depth (a delete locks <= 2 nodes/level).
+uint32_t events_per_op(bh_heap* h) {
+    unsigned levels = 64u - (unsigned)__builtin_clzll(h->slot_count);
+    return 8 + 6 * levels;
+}
+
+int prepare_record(bh_heap* h, uint64_t n_ops, cudaStream_t s, RunView& rv) {
+    if (!(h->flags & BH_FLAG_RECORD)) return BH_OK;
+    uint32_t per = events_per_op(h);
+    if (n_ops > h->ev_cap_ops || per != h->ev_per_op) {
+        cudaFree(h->d_events);
+        cudaFree(h->d_event_counts);
+        h->d_events = nullptr;
+        h->d_event_counts = nullptr;
+        BH_CUDA(cudaMalloc(&h->d_events, std::max<uint64_t>(n_ops, 1) * per * sizeof(DevEvent)));
+        BH_CUDA(cudaMalloc(&h->d_event_counts, std::max<uint64_t>(n_ops, 1) * sizeof(uint32_t)));
+        h->ev_cap_ops = n_ops;
+        h->ev_per_op = per;
+    }
+    BH_CUDA(cudaMemsetAsync(h->d_event_counts, 0, n_ops * sizeof(uint32_t), s));
+    rv.events = h->d_events;
+    rv.event_counts = h->d_event_counts;
+    rv.ev_per_op = per;
+    h->last_run_ops = n_ops;
+    return BH_OK;
+}
+
+OpCtx* get_ctx(bh_heap* h) {
+    {
+        std::lock_guard<std::mutex> g(h->ctx_mu);
+        if (!h->free_ctx.empty()) {
+            OpCtx* c = h->free_ctx.back();
+            h->free_ctx.pop_back();
+            return c;
+        }
+    }
+    OpCtx* c = new OpCtx();
+    CtxLayout lay((size_t)h->k * h->key_size);
+    c->bytes = lay.out + (size_t)h->k * h->key_size;
+    if (cudaSetDevice(h->device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMallocHost(&c->h, c->bytes) != cudaSuccess || cudaMalloc(&c->d, c->bytes) != cudaSuccess) {
+        delete c;
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> g(h->ctx_mu);
+    h->all_ctx.push_back(c);
+    return c;
+}
+
+void put_ctx(bh_heap* h, OpCtx* c) {
+    std::lock_guard<std::mutex> g(h->ctx_mu);
+    h->free_ctx.push_back(c);
+}
+
+// One operation through its own context (bh_insert / bh_delete_min).
+int single_op(bh_heap* h, const bh_op& op, const void* keys, uint32_t n, void* out, uint32_t* n_out) {
+    if (h->flags & BH_FLAG_RECORD)
+        return fail(BH_E_CONFIG, "single-op calls are not recorded; use bh_run_ops on RECORD handles");
+    OpCtx* c = get_ctx(h);
+    if (!c) return fail(BH_E_CUDA, "cannot allocate op context");
+    CtxLayout lay((size_t)h->k * h->key_size);
+    std::memcpy(c->h + lay.op, &op, sizeof(op));
+    std::memset(c->h + lay.ticket, 0, 8);
+    size_t up = lay.keys;
+    if (keys) {
+        std::memcpy(c->h + lay.keys, keys, (size_t)n * h->key_size);
+        up = lay.keys + (size_t)n * h->key_size;
+    }
+    cudaError_t e = cudaMemcpyAsync(c->d, c->h, up, cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) {
+        put_ctx(h, c);
+        return cuda_fail(e, "single_op H2D");
+    }
+    RunView rv{};
+    rv.ops = reinterpret_cast<const bh_op*>(c->d + lay.op);
+    rv.n_ops = 1;
+    rv.key_pool = c->d + lay.keys;
+    rv.out_pool = c->d + lay.out;
+    rv.out_status = reinterpret_cast<uint32_t*>(c->d + lay.status);
+    rv.out_lens = reinterpret_cast<uint32_t*>(c->d + lay.lens);
+    rv.out_seq = reinterpret_cast<unsigned long long*>(c->d + lay.seq);
+    rv.ticket = reinterpret_cast<unsigned long long*>(c->d + lay.ticket);
+    int rc = launch_ops(h, rv, 1, c->stream);
+    if (rc != BH_OK) {
+        put_ctx(h, c);
+        return rc;
+    }
+    const size_t down_end = out ? lay.out + (size_t)h->k * h->key_size : lay.keys;
+    e = cudaMemcpyAsync(c->h + lay.status, c->d + lay.status, down_end - lay.status,
+                        cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        put_ctx(h, c);
+        return cuda_fail(e, "single_op run");
+    }
+    uint32_t st, len;
+    std::memcpy(&st, c->h + lay.status, 4);
+    std::memcpy(&len, c->h + lay.lens, 4);
+    if (out && st == BH_OK) std::memcpy(out, c->h + lay.out, (size_t)len * h->key_size);
+    if (n_out) *n_out = st == BH_OK ? len : 0;
+    put_ctx(h, c);
+    switch (st) {
+        case BH_OK:
+            return BH_OK;
+        case BH_E_CAPACITY:
+            return fail(st, "heap full: " + std::to_string(h->max_nodes) + " nodes");
+        case BH_E_EMPTY:
+            return fail(st, "delete_min: heap empty");
+        case BH_E_INVALID_KEY:
+            return fail(st, "sort_batch: key reaches sentinel");
+        default:
+            return fail(BH_E_INTERNAL, "unexpected device status " + std::to_string(st));
+    }
+}
+
+bool key_at_sentinel(const bh_heap* h, const void* keys, uint32_t n) {
+    if (h->key_bits == 32) {
+        const uint32_t* p = static_cast<const uint32_t*>(keys);
+        for (uint32_t i = 0; i < n; ++i)
+            if (p[i] == 0xFFFFFFFFu) return true;
+    } else {
+        const uint64_t* p = static_cast<const uint64_t*>(keys);
+        for (uint32_t i = 0; i < n; ++i)
+            if (p[i] == ~0ull) return true;
+    }
+    return false;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bh_last_error(void) { return g_err.c_str(); }
+
+const char* bh_build_info(void) {
+    return "batchheap_b200: sm_100a, persistent CTA-per-op heap kernel, keys u32/u64, k 1..2048";
+}
+
+uint64_t bh_slot_for_rank(uint64_t rank) { return rank ? slot_for_rank(rank) : 0; }
+
+uint64_t bh_bit_reverse(uint64_t x, unsigned bits) {
+    uint64_t out = 0;
+    for (unsigned i = 0; i < bits; ++i) {
+        out = (out << 1) | (x & 1);
+        x >>= 1;
+    }
+    return out;
+}
+
+int bh_create(bh_heap** out, int variant, uint32_t k, uint32_t max_nodes, uint32_t key_bits,
+              uint32_t flags, int device) {
+    if (!out) return fail(BH_E_CONFIG, "null handle pointer");
+    *out = nullptr;
+    if (variant != BH_TD && variant != BH_BU) return fail(BH_E_CONFIG, "variant must be TD or BU");
+    if (!valid_k(k))
+        return fail(BH_E_CONFIG, "node capacity must be a power of two in [1,2048], got " + std::to_string(k));
+    if (max_nodes < 1 || max_nodes > (1u << 30)) return fail(BH_E_CONFIG, "max_nodes must be in [1, 2^30]");
+    if (key_bits != 32 && key_bits != 64) return fail(BH_E_CONFIG, "key_bits must be 32 or 64");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(BH_E_CUDA, "no CUDA device: the batched heap has no CPU fallback");
+    if (device < 0 || device >= ndev) return fail(BH_E_CONFIG, "device index out of range");
+    BH_CUDA(cudaSetDevice(device));
+
+    bh_heap* h = new bh_heap();
+    h->device = device;
+    h->variant = variant;
+    h->k = k;
+    h->key_bits = key_bits;
+    h->key_size = key_bits / 8;
+    h->max_nodes = max_nodes;
+    h->flags = flags;
+    unsigned bw = 64u - (unsigned)__builtin_clzll((unsigned long long)max_nodes);
+    h->slot_count = (1ull << bw) - 1;  // whole levels (heap.cpp:56-58)
+
+    auto cleanup = [&](int rc) {
+        bh_destroy(h);
+        return rc;
+    };
+    const size_t key_bytes = (size_t)h->slot_count * k * h->key_size;
+    cudaError_t e;
+    if ((e = cudaMalloc(&h->d_keys, key_bytes)) != cudaSuccess) return cleanup(cuda_fail(e, "keys"));
+    if ((e = cudaMalloc(&h->d_states, (h->slot_count + 1) * kStateStride * 4)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "states"));
+    if ((e = cudaMalloc(&h->d_hdr, sizeof(Header))) != cudaSuccess) return cleanup(cuda_fail(e, "hdr"));
+    if ((e = cudaMalloc(&h->d_partial, std::max<size_t>((size_t)k * h->key_size, 16))) != cudaSuccess)
+        return cleanup(cuda_fail(e, "partial"));
+    if ((e = cudaMalloc(&h->d_counters, kNumCounters * 8)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "counters"));
+    if ((e = cudaMalloc(&h->d_tickets, kTicketRing * 128)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "tickets"));
+    if ((e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "stream"));
+    if ((e = cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "aux stream"));
+    // sentinel fill (heap.cpp:58), all AVAIL (heap.cpp:59-61)
+    cudaMemsetAsync(h->d_keys, 0xFF, key_bytes, h->stream);
+    cudaMemsetAsync(h->d_states, 0, (h->slot_count + 1) * kStateStride * 4, h->stream);
+    cudaMemsetAsync(h->d_hdr, 0, sizeof(Header), h->stream);
+    cudaMemsetAsync(h->d_partial, 0xFF, std::max<size_t>((size_t)k * h->key_size, 16), h->stream);
+    cudaMemsetAsync(h->d_counters, 0, kNumCounters * 8, h->stream);
+    if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) return cleanup(cuda_fail(e, "init"));
+    int rc = key_bits == 32 ? info_u32(k, &h->kinfo) : info_u64(k, &h->kinfo);
+    if (rc != BH_OK) return cleanup(fail(rc, "kernel occupancy query failed"));
+    cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
+    h->max_ctas = (uint32_t)std::max(1, h->kinfo.max_ctas_per_sm) * (uint32_t)h->sm_count;
+    *out = h;
+    return BH_OK;
+}
+
+void bh_destroy(bh_heap* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (OpCtx* c : h->all_ctx) {
+        if (c->stream) {
+            cudaStreamSynchronize(c->stream);
+            cudaStreamDestroy(c->stream);
+        }
+        cudaFreeHost(c->h);
+        cudaFree(c->d);
+        delete c;
+    }
+    cudaFree(h->d_keys);
+    cudaFree(h->d_states);
+    cudaFree(h->d_hdr);
+    cudaFree(h->d_partial);
+    cudaFree(h->d_counters);
+    cudaFree(h->d_tickets);
+    cudaFree(h->d_stage);
+    cudaFree(h->d_events);
+    cudaFree(h->d_event_counts);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->aux) cudaStreamDestroy(h->aux);
+    delete h;
+}
+
+int bh_insert(bh_heap* h, const void* keys, uint32_t n) {
+    if (!h) return fail(BH_E_CONFIG, "null heap");
+    if (n == 0) return fail(BH_E_CAPACITY, "sort_batch: empty input");
+    if (n > h->k)
+        return fail(BH_E_CAPACITY, "sort_batch: " + std::to_string(n) + " keys exceed node capacity " +
+                                       std::to_string(h->k));
+    if (key_at_sentinel(h, keys, n)) return fail(BH_E_INVALID_KEY, "sort_batch: key reaches sentinel");
+    bh_op op{BH_OP_INSERT, n, 0};
+    return single_op(h, op, keys, n, nullptr, nullptr);
+}
+
+int bh_delete_min(bh_heap* h, void* out, uint32_t* n_out) {
+    if (!h || !out) return fail(BH_E_CONFIG, "null argument");
+    bh_op op{BH_OP_DELETE, 0, 0};
+    return single_op(h, op, nullptr, 0, out, n_out);
+}
+
+int bh_run_ops_device(bh_heap* h, const bh_op* ops, uint64_t n_ops, const void* key_pool, void* out_pool,
+                      uint32_t* out_status, uint32_t* out_lens, uint64_t* out_seq, const bh_run_cfg* cfg) {
+    if (!h) return fail(BH_E_CONFIG, "null heap");
+    if (n_ops == 0) return BH_OK;
+    cudaStream_t s = (cfg && cfg->stream) ? static_cast<cudaStream_t>(cfg->stream) : h->stream;
+    BH_CUDA(cudaSetDevice(h->device));
+    RunView rv{};
+    rv.ops = ops;
+    rv.n_ops = n_ops;
+    rv.key_pool = key_pool;
+    rv.out_pool = out_pool;
+    rv.out_status = out_status;
+    rv.out_lens = out_lens;
+    rv.out_seq = reinterpret_cast<unsigned long long*>(out_seq);
+    const uint32_t slot = h->ticket_next.fetch_add(1) % kTicketRing;
+    rv.ticket = h->d_tickets + slot * 16;
+    BH_CUDA(cudaMemsetAsync(rv.ticket, 0, 8, s));
+    if (h->flags & BH_FLAG_RECORD) {
+        std::lock_guard<std::mutex> g(h->rec_mu);
+        int rc = prepare_record(h, n_ops, s, rv);
+        if (rc != BH_OK) return rc;
+        return launch_ops(h, rv, pick_ctas(h, n_ops, cfg), s);
+    }
+    return launch_ops(h, rv, pick_ctas(h, n_ops, cfg), s);
+}
+
+int bh_run_ops(bh_heap* h, const bh_op* ops, uint64_t n_ops, const void* key_pool, uint64_t key_pool_len,
+               void* out_pool, uint64_t out_pool_len, uint32_t* out_status, uint32_t* out_lens,
+               uint64_t* out_seq, const bh_run_cfg* cfg) {
+    if (!h) return fail(BH_E_CONFIG, "null heap");
+    if (n_ops == 0) return BH_OK;
+    for (uint64_t i = 0; i < n_ops; ++i) {
+        const bh_op& o = ops[i];
+        if (o.kind == BH_OP_INSERT) {
+            if ((uint64_t)o.offset + o.len > key_pool_len)
+                return fail(BH_E_CONFIG, "insert op " + std::to_string(i) + " reads past key_pool");
+        } else if (o.kind == BH_OP_DELETE) {
+            if ((uint64_t)o.offset + h->k > out_pool_len)
+                return fail(BH_E_CONFIG, "delete op " + std::to_string(i) + " writes past out_pool");
+        } else {
+            return fail(BH_E_CONFIG, "unknown op kind");
+        }
+    }
+    std::lock_guard<std::mutex> g(h->bulk_mu);
+    BH_CUDA(cudaSetDevice(h->device));
+    cudaStream_t s = (cfg && cfg->stream) ? static_cast<cudaStream_t>(cfg->stream) : h->stream;
+    auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t ops_b = align(n_ops * sizeof(bh_op));
+    const size_t pool_b = align(std::max<uint64_t>(key_pool_len, 1) * h->key_size);
+    const size_t out_b = align(std::max<uint64_t>(out_pool_len, 1) * h->key_size);
+    const size_t st_b = align(n_ops * 4);
+    const size_t seq_b = align(n_ops * 8);
+    const size_t need = ops_b + pool_b + out_b + 2 * st_b + seq_b;
+    if (need > h->stage_bytes) {
+        cudaFree(h->d_stage);
+        h->d_stage = nullptr;
+        BH_CUDA(cudaMalloc(&h->d_stage, need));
+        h->stage_bytes = need;
+    }
+    unsigned char* base = static_cast<unsigned char*>(h->d_stage);
+    bh_op* d_ops = reinterpret_cast<bh_op*>(base);
+    void* d_pool = base + ops_b;
+    void* d_out = base + ops_b + pool_b;
+    uint32_t* d_status = reinterpret_cast<uint32_t*>(base + ops_b + pool_b + out_b);
+    uint32_t* d_lens = reinterpret_cast<uint32_t*>(base + ops_b + pool_b + out_b + st_b);
+    uint64_t* d_seq = reinterpret_cast<uint64_t*>(base + ops_b + pool_b + out_b + 2 * st_b);
+    BH_CUDA(cudaMemcpyAsync(d_ops, ops, n_ops * sizeof(bh_op), cudaMemcpyHostToDevice, s));
+    if (key_pool && key_pool_len)
+        BH_CUDA(cudaMemcpyAsync(d_pool, key_pool, key_pool_len * h->key_size, cudaMemcpyHostToDevice, s));
+    bh_run_cfg c2 = cfg ? *cfg : bh_run_cfg{0, 0, nullptr};
+    c2.stream = s;
+    int rc = bh_run_ops_device(h, d_ops, n_ops, d_pool, d_out, d_status, d_lens, d_seq, &c2);
+    if (rc != BH_OK) return rc;
+    if (out_pool && out_pool_len)
+        BH_CUDA(cudaMemcpyAsync(out_pool, d_out, out_pool_len * h->key_size, cudaMemcpyDeviceToHost, s));
+    if (out_status) BH_CUDA(cudaMemcpyAsync(out_status, d_status, n_ops * 4, cudaMemcpyDeviceToHost, s));
+    if (out_lens) BH_CUDA(cudaMemcpyAsync(out_lens, d_lens, n_ops * 4, cudaMemcpyDeviceToHost, s));
+    if (out_seq) BH_CUDA(cudaMemcpyAsync(out_seq, d_seq, n_ops * 8, cudaMemcpyDeviceToHost, s));
+    BH_CUDA(cudaStreamSynchronize(s));
+    return BH_OK;
+}
+
+int bh_plan_phase(bh_heap* h, int kind, uint64_t n_keys, bh_op* ops, int on_device, void* stream) {
+    if (!h) return fail(BH_E_CONFIG, "null heap");
+    const uint64_t n_ops = (n_keys + h->k - 1) / h->k;
+    if (!on_device) {
+        for (uint64_t i = 0; i < n_ops; ++i) {
+            ops[i].kind = kind == 0 ? BH_OP_INSERT : BH_OP_DELETE;
+            const uint64_t at = i * h->k;
+            ops[i].len = kind == 0 ? (uint32_t)std::min<uint64_t>(h->k, n_keys - at) : 0;
+            ops[i].offset = at;
+        }
+        return BH_OK;
+    }
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+    if (n_ops == 0) return BH_OK;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n_ops + 255) / 256, 148 * 8);
+    plan_kernel<<<grid, 256, 0, s>>>(kind, h->k, n_keys, n_ops, ops);
+    BH_CUDA(cudaGetLastError());
+    return BH_OK;
+}
+
+int bh_peek_stats(bh_heap* h, bh_peek* out) {
+    if (!h || !out) return fail(BH_E_CONFIG, "null argument");
+    Header hd;
+    BH_CUDA(cudaSetDevice(h->device));
+    BH_CUDA(cudaMemcpyAsync(&hd, h->d_hdr, sizeof(Header), cudaMemcpyDeviceToHost, h->aux));
+    BH_CUDA(cudaStreamSynchronize(h->aux));
+    out->node_count = hd.node_count;
+    out->partial_len = hd.partial_len;
+    out->key_count = hd.node_count * h->k + hd.partial_len;
+    out->level_count = hd.node_count ? 64u - (unsigned)__builtin_clzll(hd.node_count) : 0;
+    return BH_OK;
+}
+
+int bh_get_counters(bh_heap* h, bh_counters* out) {
+    if (!h || !out) return fail(BH_E_CONFIG, "null argument");
+    unsigned long long c[kNumCounters];
+    BH_CUDA(cudaSetDevice(h->device));
+    BH_CUDA(cudaMemcpyAsync(c, h->d_counters, sizeof(c), cudaMemcpyDeviceToHost, h->aux));
+    BH_CUDA(cudaStreamSynchronize(h->aux));
+    out->inserts = c[cInserts];
+    out->deletes = c[cDeletes];
+    out->merges = c[cMerges];
+    out->elided_merges = c[cElided];
+    out->early_stops = c[cEarlyStops];
+    out->propagation_node_visits = c[cVisits];
+    out->coop_handoffs = c[cCoop];
+    out->max_partial_len = c[cMaxPartial];
+    return BH_OK;
+}
+
+int bh_reset_counters(bh_heap* h) {
+    if (!h) return fail(BH_E_CONFIG, "null heap");
+    BH_CUDA(cudaSetDevice(h->device));
+    BH_CUDA(cudaMemsetAsync(h->d_counters, 0, kNumCounters * 8, h->aux));
+    BH_CUDA(cudaStreamSynchronize(h->aux));
+    return BH_OK;
+}
+
+int bh_select_insert_target(bh_heap* h, uint64_t* slot) {
+    bh_peek p;
+    int rc = bh_peek_stats(h, &p);
+    if (rc) return rc;
+    if (p.node_count == h->max_nodes) return fail(BH_E_CAPACITY, "heap full");
+    *slot = slot_for_rank(p.node_count + 1);
+    return BH_OK;
+}
+
+int bh_collect_resident(bh_heap* h, void* out, uint64_t cap, uint64_t* n_out) {
+    if (!h || !n_out) return fail(BH_E_CONFIG, "null argument");
+    BH_CUDA(cudaSetDevice(h->device));
+    Header hd;
+    BH_CUDA(cudaMemcpyAsync(&hd, h->d_hdr, sizeof(Header), cudaMemcpyDeviceToHost, h->aux));
+    BH_CUDA(cudaStreamSynchronize(h->aux));
+    const uint64_t n = hd.node_count * h->k + hd.partial_len;
+    *n_out = n;
+    if (!out) return BH_OK;
+    if (cap < n) return fail(BH_E_CAPACITY, "collect_resident: output too small");
+    const size_t node_bytes = (size_t)hd.node_count * h->k * h->key_size;
+    if (node_bytes) {
+        void* d_tmp = nullptr;
+        BH_CUDA(cudaMalloc(&d_tmp, node_bytes));
+        HeapView hv = h->view();
+        int rc = h->key_bits == 32 ? gather_u32(hv, hd.node_count, d_tmp, h->aux)
+                                   : gather_u64(hv, hd.node_count, d_tmp, h->aux);
+        if (rc != BH_OK) {
+            cudaFree(d_tmp);
+            return fail(rc, "gather launch failed");
+        }
+        cudaError_t e = cudaMemcpyAsync(out, d_tmp, node_bytes, cudaMemcpyDeviceToHost, h->aux);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->aux);
+        cudaFree(d_tmp);
+        if (e != cudaSuccess) return cuda_fail(e, "collect_resident");
+    }
+    if (hd.partial_len)
+        BH_CUDA(cudaMemcpy(static_cast<unsigned char*>(out) + node_bytes, h->d_partial,
+                           hd.partial_len * h->key_size, cudaMemcpyDeviceToHost));
+    return BH_OK;
+}
+
+int bh_check_invariants(bh_heap* h, int* ok, char* detail, size_t cap) {
+    if (!h || !ok) return fail(BH_E_CONFIG, "null argument");
+    BH_CUDA(cudaSetDevice(h->device));
+    std::string msg;
+    unsigned long long* d_res = nullptr;
+    BH_CUDA(cudaMalloc(&d_res, 4 * 8));
+    unsigned long long init[4] = {0, ~0ull, 0, 0};
+    BH_CUDA(cudaMemcpy(d_res, init, sizeof(init), cudaMemcpyHostToDevice));
+    HeapView hv = h->view();
+    int rc = h->key_bits == 32 ? check_u32(hv, d_res, h->aux) : check_u64(hv, d_res, h->aux);
+    unsigned long long res[4];
+    cudaError_t e = cudaMemcpyAsync(res, d_res, sizeof(res), cudaMemcpyDeviceToHost, h->aux);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->aux);
+    cudaFree(d_res);
+    if (rc != BH_OK || e != cudaSuccess) return cuda_fail(e, "check kernel");
+    if (res[0]) {
+        static const char* names[] = {"state != AVAIL at quiescence", "unoccupied slot holds keys",
+                                      "unsorted node (property 2)", "node contains sentinel",
+                                      "parent unoccupied", "property 1 violated"};
+        msg += std::to_string(res[0]) + " bad slots, first " + std::to_string(res[1]) + ":";
+        for (int b = 0; b < 6; ++b)
+            if (res[2] & (1ull << b)) msg += std::string(" ") + names[b] + ";";
+    }
+    // partial buffer: sorted, <= k-1, dominates the root (property 3)
+    Header hd;
+    BH_CUDA(cudaMemcpy(&hd, h->d_hdr, sizeof(Header), cudaMemcpyDeviceToHost));
+    std::vector<unsigned char> part((size_t)h->k * h->key_size);
+    std::vector<unsigned char> root((size_t)h->k * h->key_size);
+    BH_CUDA(cudaMemcpy(part.data(), h->d_partial, part.size(), cudaMemcpyDeviceToHost));
+    BH_CUDA(cudaMemcpy(root.data(), h->d_keys, root.size(), cudaMemcpyDeviceToHost));
+    auto keyat = [&](const std::vector<unsigned char>& v, size_t i) -> uint64_t {
+        if (h->key_bits == 32) return reinterpret_cast<const uint32_t*>(v.data())[i];
+        return reinterpret_cast<const uint64_t*>(v.data())[i];
+    };
+    if (hd.partial_len > h->k - 1) msg += " partial buffer overflow;";
+    for (uint64_t i = 1; i < hd.partial_len && i < h->k; ++i)
+        if (keyat(part, i - 1) > keyat(part, i)) {
+            msg += " partial buffer unsorted;";
+            break;
+        }
+    if (hd.node_count >= 1 && hd.partial_len && keyat(part, 0) < keyat(root, h->k - 1))
+        msg += " property 3 violated;";
+    if (hd.error_flags) msg += " device error flags " + std::to_string(hd.error_flags) + ";";
+    *ok = msg.empty() ? 1 : 0;
+    if (detail && cap) {
+        std::strncpy(detail, msg.c_str(), cap - 1);
+        detail[cap - 1] = 0;
+    }
+    return BH_OK;
+}
+
+int bh_dump(bh_heap* h, void* keys_out, uint64_t keys_cap, void* partial_out, uint32_t* partial_len,
+            uint32_t* states_out) {
+    if (!h) return fail(BH_E_CONFIG, "null heap");
+    BH_CUDA(cudaSetDevice(h->device));
+    BH_CUDA(cudaStreamSynchronize(h->stream));
+    const uint64_t n = h->slot_count * h->k;
+    if (keys_out) {
+        if (keys_cap < n) return fail(BH_E_CAPACITY, "dump: keys_out too small");
+        BH_CUDA(cudaMemcpy(keys_out, h->d_keys, n * h->key_size, cudaMemcpyDeviceToHost));
+    }
+    Header hd;
+    BH_CUDA(cudaMemcpy(&hd, h->d_hdr, sizeof(Header), cudaMemcpyDeviceToHost));
+    if (partial_len) *partial_len = (uint32_t)hd.partial_len;
+    if (partial_out && hd.partial_len)
+        BH_CUDA(cudaMemcpy(partial_out, h->d_partial, hd.partial_len * h->key_size, cudaMemcpyDeviceToHost));
+    if (states_out) {
+        std::vector<uint32_t> raw((h->slot_count + 1) * kStateStride);
+        BH_CUDA(cudaMemcpy(raw.data(), h->d_states, raw.size() * 4, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i <= h->slot_count; ++i) states_out[i] = raw[i * kStateStride];
+    }
+    return BH_OK;
+}
+
+int bh_info(bh_heap* h, uint32_t* k, uint32_t* key_bits, uint64_t* slot_count, uint32_t* max_nodes,
+            int* variant, uint32_t* threads_per_cta, uint32_t* max_ctas) {
+    if (!h) return fail(BH_E_CONFIG, "null heap");
+    if (k) *k = h->k;
+    if (key_bits) *key_bits = h->key_bits;
+    if (slot_count) *slot_count = h->slot_count;
+    if (max_nodes) *max_nodes = h->max_nodes;
+    if (variant) *variant = h->variant;
+    if (threads_per_cta) *threads_per_cta = h->kinfo.threads;
+    if (max_ctas) *max_ctas = h->max_ctas;
+    return BH_OK;
+}
+
+int bh_history(bh_heap* h, bh_event* out, uint64_t cap, uint64_t* n_out) {
+    if (!h || !n_out) return fail(BH_E_CONFIG, "null argument");
+    if (!(h->flags & BH_FLAG_RECORD)) return fail(BH_E_CONFIG, "heap was not created with BH_FLAG_RECORD");
+    std::lock_guard<std::mutex> g(h->rec_mu);
+    BH_CUDA(cudaSetDevice(h->device));
+    BH_CUDA(cudaDeviceSynchronize());
+    const uint64_t ops = h->last_run_ops;
+    std::vector<uint32_t> counts(ops);
+    std::vector<DevEvent> ev(ops * h->ev_per_op);
+    if (ops) {
+        BH_CUDA(cudaMemcpy(counts.data(), h->d_event_counts, ops * 4, cudaMemcpyDeviceToHost));
+        BH_CUDA(cudaMemcpy(ev.data(), h->d_events, ev.size() * sizeof(DevEvent), cudaMemcpyDeviceToHost));
+    }
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < ops; ++i) total += counts[i];
+    *n_out = total;
+    if (!out) return BH_OK;
+    if (cap < total) return fail(BH_E_CAPACITY, "history: output too small");
+    uint64_t at = 0;
+    for (uint64_t i = 0; i < ops; ++i)
+        for (uint32_t j = 0; j < counts[i]; ++j) {
+            const DevEvent& d = ev[i * h->ev_per_op + j];
+            out[at].ts = d.ts;
+            out[at].op = d.op;
+            out[at].kind = d.kind;
+            out[at].pad = 0;
+            out[at].node = d.node;
+            ++at;
+        }
+    return BH_OK;
+}
+
+int bh_sort_batches(uint32_t key_bits, uint32_t k, void* keys, const uint32_t* lens, uint64_t batches,
+                    void* stream) {
+    if (!valid_k(k) || (key_bits != 32 && key_bits != 64)) return fail(BH_E_CONFIG, "bad k or key_bits");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc = key_bits == 32 ? sort_u32(k, keys, lens, batches, s) : sort_u64(k, keys, lens, batches, s);
+    return rc == BH_OK ? rc : fail(rc, "sort launch failed");
+}
+
+int bh_merge_split(uint32_t key_bits, uint32_t k, const void* a, const void* b, void* hi, void* lo,
+                   uint64_t pairs, void* stream) {
+    if (!valid_k(k) || (key_bits != 32 && key_bits != 64)) return fail(BH_E_CONFIG, "bad k or key_bits");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc = key_bits == 32 ? merge_u32(k, a, b, hi, lo, pairs, s) : merge_u64(k, a, b, hi, lo, pairs, s);
+    return rc == BH_OK ? rc : fail(rc, "merge launch failed");
+}
+
+int bh_generate_keys(int order, uint64_t n, uint64_t seed, uint32_t key_bits, void* out) {
+    if (!out && n) return fail(BH_E_CONFIG, "null output");
+    if (key_bits != 32 && key_bits != 64) return fail(BH_E_CONFIG, "key_bits must be 32 or 64");
+    auto put = [&](uint64_t i, uint64_t v) {
+        if (key_bits == 32)
+            static_cast<uint32_t*>(out)[i] = (uint32_t)v;
+        else
+            static_cast<uint64_t*>(out)[i] = v;
+    };
+    switch (order) {
+        case 0: {
+            std::mt19937_64 rng(seed);
+            std::uniform_int_distribution<uint64_t> dist(0, (uint64_t{1} << 32) - 1);
+            for (uint64_t i = 0; i < n; ++i) put(i, dist(rng));
+            return BH_OK;
+        }
+        case 1:
+            for (uint64_t i = 0; i < n; ++i) put(i, i);
+            return BH_OK;
+        case 2:
+            for (uint64_t i = 0; i < n; ++i) put(i, n - i);
+            return BH_OK;
+    }
+    return fail(BH_E_CONFIG, "order must be 0 (random), 1 (ascend) or 2 (descend)");
+}
+
+}  // extern "C"

@@ -1,0 +1,278 @@
+// bh_device.cuh -- CTA-level primitives of the batched generalized heap for
+// sm_100a: multi-state node locks in HBM, coalesced node moves, the block
+// bitonic sort and the merge-path MergeAndSort.
+//
+// One thread block owns one heap operation (section 4: "threads in
+// one thread block work together for one INS and DEL operation"); lock words
+// are driven by a single elected thread and the decision is broadcast through
+// shared memory with a barrier, so warps never diverge on a lock.
+#pragma once
+
+#include <cstdint>
+
+#include "bh_internal.h"
+
+namespace bh {
+
+template <typename Key>
+struct KeyLimits;
+template <>
+struct KeyLimits<uint32_t> {
+    static constexpr uint32_t kMax = 0xFFFFFFFFu;
+};
+template <>
+struct KeyLimits<unsigned long long> {
+    static constexpr unsigned long long kMax = ~0ull;
+};
+
+// ---------------------------------------------------------------- locks --
+// GPU-scope acquire/release on the node state words (reference
+// proj/src/heap.cpp:87-114 uses std::atomic acq_rel CAS + release store).
+__device__ __forceinline__ uint32_t state_load(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ bool state_cas(uint32_t* p, uint32_t expected, uint32_t desired) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.cas.b32 %0, [%1], %2, %3;"
+                 : "=r"(old)
+                 : "l"(p), "r"(expected), "r"(desired)
+                 : "memory");
+    return old == expected;
+}
+
+__device__ __forceinline__ void state_store_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Spin backoff (reference Backoff, proj/src/heap.cpp:18-31: 2^0..2^5 pause
+// rounds, then yield).  On the GPU a waiting CTA sleeps in growing steps so the
+// lock holder's SM and the contended L2 slice stay free.
+struct Backoff {
+    uint32_t ns = 0;
+    __device__ __forceinline__ void pause() {
+        ns = ns == 0 ? 20 : (ns < 320 ? ns * 2 : ns);
+        __nanosleep(ns);
+    }
+};
+
+// ------------------------------------------------------------ L2 access --
+// Heap data is shared across SMs whose L1s are not coherent: all node reads
+// go through L2 (ld.global.cg) and all node writes are st.global.cg.
+__device__ __forceinline__ unsigned long long ld_cg_u64(const unsigned long long* p) {
+    return __ldcg(p);
+}
+__device__ __forceinline__ void st_cg_u64(unsigned long long* p, unsigned long long v) {
+    __stcg(p, v);
+}
+
+template <typename Key>
+__device__ __forceinline__ Key ld_key(const Key* p) {
+    return __ldcg(p);
+}
+template <typename Key>
+__device__ __forceinline__ void st_key(Key* p, Key v) {
+    __stcg(p, v);
+}
+
+// CTA-cooperative copies of n keys.  16-byte vectors when both sides are
+// aligned and the byte count is a multiple of 16 (always true for node copies
+// with k*sizeof(Key) >= 16), scalar otherwise.  No barrier inside.
+template <typename Key, int T>
+__device__ __forceinline__ void cta_load(Key* __restrict__ s, const Key* __restrict__ g, uint32_t n) {
+    const uint32_t bytes = n * (uint32_t)sizeof(Key);
+    if (((bytes | (uint32_t)(uintptr_t)g) & 15u) == 0) {
+        const uint4* gv = reinterpret_cast<const uint4*>(g);
+        uint4* sv = reinterpret_cast<uint4*>(s);
+        for (uint32_t i = threadIdx.x; i < bytes / 16; i += T) sv[i] = __ldcg(gv + i);
+    } else {
+        for (uint32_t i = threadIdx.x; i < n; i += T) s[i] = ld_key(g + i);
+    }
+}
+
+template <typename Key, int T>
+__device__ __forceinline__ void cta_store(Key* __restrict__ g, const Key* __restrict__ s, uint32_t n) {
+    const uint32_t bytes = n * (uint32_t)sizeof(Key);
+    if (((bytes | (uint32_t)(uintptr_t)g) & 15u) == 0) {
+        uint4* gv = reinterpret_cast<uint4*>(g);
+        const uint4* sv = reinterpret_cast<const uint4*>(s);
+        for (uint32_t i = threadIdx.x; i < bytes / 16; i += T) __stcg(gv + i, sv[i]);
+    } else {
+        for (uint32_t i = threadIdx.x; i < n; i += T) st_key(g + i, s[i]);
+    }
+}
+
+// Global -> global (partial buffer to a delete result).
+template <typename Key, int T>
+__device__ __forceinline__ void cta_copy_gg(Key* __restrict__ dst, const Key* __restrict__ src, uint32_t n) {
+    for (uint32_t i = threadIdx.x; i < n; i += T) st_key(dst + i, ld_key(src + i));
+}
+
+template <typename Key, int T>
+__device__ __forceinline__ void cta_fill(Key* g, Key v, uint32_t n) {
+    const uint32_t bytes = n * (uint32_t)sizeof(Key);
+    if (((bytes | (uint32_t)(uintptr_t)g) & 15u) == 0) {
+        uint4 fill;
+        fill.x = fill.y = fill.z = fill.w = 0xFFFFFFFFu;  // v is always the all-ones sentinel
+        uint4* gv = reinterpret_cast<uint4*>(g);
+        for (uint32_t i = threadIdx.x; i < bytes / 16; i += T) __stcg(gv + i, fill);
+    } else {
+        for (uint32_t i = threadIdx.x; i < n; i += T) st_key(g + i, v);
+    }
+}
+
+// ------------------------------------------------------------- sorting --
+// Block bitonic sort of K keys in shared memory (section 4.1).  The
+// stages whose compare distance stays inside one thread's register pair are
+// done in registers; the wider ones go through shared memory.  Ends with a
+// barrier.  Caller pads unused tail slots with the sentinel.
+template <typename Key, int K, int T>
+__device__ __forceinline__ void cta_bitonic_sort(Key* s) {
+    if constexpr (K >= 2) {
+        constexpr uint32_t kPairs = K / 2;
+#pragma unroll 1
+        for (uint32_t size = 2; size <= K; size <<= 1) {
+#pragma unroll 1
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t p = threadIdx.x; p < kPairs; p += T) {
+                    const uint32_t i = 2 * p - (p & (stride - 1));
+                    const uint32_t j = i + stride;
+                    const bool up = (i & size) == 0;
+                    const Key a = s[i];
+                    const Key b = s[j];
+                    if ((a > b) == up) {
+                        s[i] = b;
+                        s[j] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    } else {
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------- merging --
+// Merge-path MergeAndSort (section 4.2, Odeh et al.): stable merge
+// of sorted A[0,na) and B[0,nb) held in shared memory; output element d goes
+// to out1[d] when d < split, else out2[d - split].  Ties take A first, as
+// the reference's merge_sorted does (proj/src/batch.cpp:21-30).  Each thread
+// binary-searches its diagonal, then merges its run in registers and writes
+// it out.  No barrier inside.
+template <typename Key, int T>
+__device__ __forceinline__ void cta_merge(const Key* __restrict__ A, uint32_t na,
+                                          const Key* __restrict__ B, uint32_t nb,
+                                          Key* __restrict__ out1, uint32_t split,
+                                          Key* __restrict__ out2) {
+    const uint32_t total = na + nb;
+    const uint32_t per = (total + T - 1) / T;
+    const uint32_t d0 = threadIdx.x * per;
+    if (d0 >= total) return;
+    const uint32_t d1 = min(d0 + per, total);
+    uint32_t lo = d0 > nb ? d0 - nb : 0;
+    uint32_t hi = min(d0, na);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (A[mid] <= B[d0 - 1 - mid])
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    uint32_t i = lo, j = d0 - lo;
+    for (uint32_t d = d0; d < d1; ++d) {
+        const bool take_a = j >= nb || (i < na && A[i] <= B[j]);
+        const Key v = take_a ? A[i++] : B[j++];
+        if (d < split)
+            out1[d] = v;
+        else
+            out2[d - split] = v;
+    }
+}
+
+// Same contract, specialised for the hot case of two full k-batches with the
+// split at k: each thread's run lies entirely in one output half, is built in
+// registers and leaves as whole 16-byte vectors when aligned.
+template <typename Key, int K, int T>
+__device__ __forceinline__ void cta_merge_full(const Key* __restrict__ A, const Key* __restrict__ B,
+                                               Key* __restrict__ out_hi, Key* __restrict__ out_lo) {
+    constexpr uint32_t kTotal = 2 * K;
+    constexpr uint32_t kPer = (kTotal + T - 1) / T;
+    const uint32_t d0 = threadIdx.x * kPer;
+    if (d0 >= kTotal) return;
+    uint32_t lo = d0 > K ? d0 - K : 0;
+    uint32_t hi = min(d0, (uint32_t)K);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (A[mid] <= B[d0 - 1 - mid])
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    uint32_t i = lo, j = d0 - lo;
+    Key run[kPer];
+#pragma unroll
+    for (uint32_t e = 0; e < kPer; ++e) {
+        const Key a = i < K ? A[i] : KeyLimits<Key>::kMax;
+        const Key b = j < K ? B[j] : KeyLimits<Key>::kMax;
+        const bool take_a = j >= K || (i < K && a <= b);
+        run[e] = take_a ? a : b;
+        i += take_a;
+        j += !take_a;
+    }
+    Key* dst = d0 < K ? out_hi + d0 : out_lo + (d0 - K);
+    constexpr uint32_t kRunBytes = kPer * sizeof(Key);
+    if constexpr (kRunBytes % 16 == 0) {
+        if (((uint32_t)(uintptr_t)dst & 15u) == 0) {
+            uint4* dv = reinterpret_cast<uint4*>(dst);
+            const uint4* rv = reinterpret_cast<const uint4*>(run);
+#pragma unroll
+            for (uint32_t v = 0; v < kRunBytes / 16; ++v) dv[v] = rv[v];
+            return;
+        }
+    }
+#pragma unroll
+    for (uint32_t e = 0; e < kPer; ++e) dst[e] = run[e];
+}
+
+// needs_merge (proj/include/batchheap/batch.hpp:61-66) on two full batches in
+// shared memory; every thread evaluates it identically.
+template <typename Key, int K>
+__device__ __forceinline__ bool needs_merge_full(const Key* a, const Key* b) {
+    if (a[K - 1] <= b[0]) return false;
+    if (b[K - 1] <= a[0]) return false;
+    return true;
+}
+
+// ------------------------------------------------------------- bitrev ----
+// proj/include/batchheap/bitrev.hpp:15-33 with the bit-reverse intrinsic.
+__host__ __device__ __forceinline__ unsigned long long slot_for_rank(unsigned long long rank) {
+#ifdef __CUDA_ARCH__
+    const unsigned level = 63u - (unsigned)__clzll((long long)rank);
+    const unsigned long long base = 1ull << level;
+    const unsigned long long off = rank - base;
+    return base + (level ? (__brevll(off) >> (64 - level)) : 0ull);
+#else
+    const unsigned level = 63u - (unsigned)__builtin_clzll(rank);
+    const unsigned long long base = 1ull << level;
+    unsigned long long off = rank - base, out = 0;
+    for (unsigned i = 0; i < level; ++i) {
+        out = (out << 1) | (off & 1);
+        off >>= 1;
+    }
+    return base + out;
+#endif
+}
+
+// Inverse of slot_for_rank (bit reversal is an involution within a level).
+__host__ __device__ __forceinline__ unsigned long long rank_for_slot(unsigned long long slot) {
+    return slot_for_rank(slot);
+}
+
+__device__ __forceinline__ unsigned level_of(unsigned long long slot) {
+    return 63u - (unsigned)__clzll((long long)slot);
+}
+
+}  // namespace bh

@@ -1,0 +1,811 @@
+// bh_heap.cuh -- the concurrent generalized heap as a persistent kernel.
+//
+// Each CTA repeatedly claims the next operation ticket and executes that whole
+// INS or DEL (section 4, "threads in one thread block work together
+// for one INS and DEL operation"), following the reference protocol
+// (proj/src/heap.cpp) state for state:
+//
+//   insert      heap.cpp:123-188   root phase: sort, partial buffer, rank
+//   insert_td   heap.cpp:218-293   TARGET claim, hand-over-hand merge walk,
+//                                  MARKED cooperation (ship_to_root :207-216)
+//   insert_bu   heap.cpp:295-407   park/INSHOLD climb, DELMOD skip, early stop
+//   do_delete   heap.cpp:420-465   root take, refill (:467-531), partial
+//                                  re-merge (:533-545), heapify (:547-667)
+//
+// B200-specific choices (not in the reference):
+//   * node data moves through shared memory; the node a walk carries stays in
+//     shared memory and is written back once, when its lock is released;
+//   * the delete's root refill is kept in shared memory until the first
+//     heapify level releases the root (no one else reads the root meanwhile);
+//   * lock words are spun on by one elected thread (ld.acquire + CAS) with
+//     __nanosleep backoff; the outcome is broadcast with one barrier;
+//   * counters are per-CTA registers folded into global memory at exit.
+//
+// Deliberate deviation: heapify's merge elision places the batch that holds
+// the smaller keys in the hi child on an equal-maxima tie (reference bug at
+// heap.cpp:628-636).
+#pragma once
+
+#include "bh_device.cuh"
+
+namespace bh {
+
+struct OpShared {
+    unsigned long long op;
+    unsigned long long nodes;
+    unsigned long long plen;
+    unsigned long long seq;
+    uint32_t act;
+    uint32_t lk, rk;        // children locked?
+    uint32_t lrel, rrel;    // children release states
+    uint32_t owned;
+};
+
+template <typename Key, int K, int T>
+struct HeapCta {
+    static constexpr Key kMaxKey = KeyLimits<Key>::kMax;
+    static constexpr int kBufs = 6;
+
+    HeapView hv;
+    RunView rv;
+    Key* keys;
+    uint32_t* states;
+    Header* hdr;
+    Key* partial;
+    OpShared* sh;
+    Key* bufs;
+    unsigned long long cnt[kNumCounters];
+    unsigned long long cur_op;
+    bool elide;
+    bool record;
+
+    __device__ __forceinline__ HeapCta(const HeapView& h, const RunView& r, unsigned char* smem,
+                                       OpShared* s)
+        : hv(h), rv(r), sh(s) {
+        keys = static_cast<Key*>(h.keys);
+        states = h.states;
+        hdr = h.hdr;
+        partial = static_cast<Key*>(h.partial);
+        bufs = reinterpret_cast<Key*>(smem);
+#pragma unroll
+        for (int i = 0; i < kNumCounters; ++i) cnt[i] = 0;
+        elide = (h.flags & BH_FLAG_ELIDE_MERGES) != 0;
+        record = (h.flags & BH_FLAG_RECORD) != 0;
+    }
+
+    __device__ __forceinline__ Key* buf(int i) const { return bufs + i * K; }
+    __device__ __forceinline__ bool leader() const { return threadIdx.x == 0; }
+    __device__ __forceinline__ Key* node(unsigned long long slot) const { return keys + (slot - 1) * K; }
+    __device__ __forceinline__ uint32_t* st(unsigned long long slot) const {
+        return states + slot * kStateStride;
+    }
+    __device__ __forceinline__ void count(int idx, unsigned long long v = 1) {
+        if (leader()) cnt[idx] += v;
+    }
+
+    // ----------------------------------------------------------- recorder --
+    // Recorder::op_begin/lock_acquired/lock_released/op_end
+    // (proj/src/instrumentation.cpp:47-107): one global device clock.
+    __device__ void rec(uint16_t kind, unsigned long long slot) {
+        if (!record || !leader()) return;
+        const unsigned long long ts = atomicAdd(&hdr->clock, 1ull);
+        const uint32_t idx = rv.event_counts[cur_op];
+        if (idx >= rv.ev_per_op) {
+            atomicOr(&hdr->error_flags, (unsigned long long)kErrEventOverflow);
+            return;
+        }
+        DevEvent& e = rv.events[cur_op * rv.ev_per_op + idx];
+        e.ts = ts;
+        e.op = (uint32_t)cur_op;
+        e.kind = kind;
+        e.pad = 0;
+        e.node = slot;
+        rv.event_counts[cur_op] = idx + 1;
+    }
+    __device__ void rec_abort() {
+        if (record && leader()) rv.event_counts[cur_op] = 0;
+    }
+
+    // -------------------------------------------------------------- locks --
+    // lock_avail (heap.cpp:98-109): AVAIL -> INUSE.  Leader only.
+    __device__ void lead_lock_avail(unsigned long long slot) {
+        uint32_t* p = st(slot);
+        Backoff b;
+        for (;;) {
+            if (state_load(p) == kAvail && state_cas(p, kAvail, kInUse)) break;
+            b.pause();
+        }
+        rec(kEvAcq, slot);
+    }
+    // unlock (heap.cpp:111-114).  Leader only; the caller has passed a
+    // barrier after the CTA's last write to data guarded by this lock.
+    __device__ void lead_unlock(unsigned long long slot, uint32_t release_as = kAvail) {
+        rec(kEvRel, slot);
+        __threadfence();
+        state_store_release(st(slot), release_as);
+    }
+    __device__ void lead_release_only(unsigned long long slot, uint32_t release_as) {
+        __threadfence();
+        state_store_release(st(slot), release_as);
+    }
+
+    __device__ void status(unsigned long long opi, uint32_t code, uint32_t len, unsigned long long seq) {
+        if (!leader()) return;
+        if (rv.out_status) rv.out_status[opi] = code;
+        if (rv.out_lens) rv.out_lens[opi] = len;
+        if (rv.out_seq) rv.out_seq[opi] = seq;
+    }
+
+    __device__ void note_partial(unsigned long long len) {
+        if (leader() && len > cnt[cMaxPartial]) cnt[cMaxPartial] = len;
+    }
+
+    // =============================================================== run ==
+    __device__ void run() {
+        for (;;) {
+            if (leader()) sh->op = atomicAdd(rv.ticket, 1ull);
+            __syncthreads();
+            const unsigned long long opi = sh->op;
+            __syncthreads();
+            if (opi >= rv.n_ops) break;
+            cur_op = opi;
+            const bh_op o = rv.ops[opi];
+            if (o.kind == BH_OP_INSERT)
+                do_insert(opi, o);
+            else
+                do_delete(opi, o);
+            __syncthreads();
+        }
+        if (leader()) {
+#pragma unroll
+            for (int i = 0; i < kNumCounters; ++i) {
+                if (i == cMaxPartial) {
+                    if (cnt[i]) atomicMax(&hv.counters[i], cnt[i]);
+                } else if (cnt[i]) {
+                    atomicAdd(&hv.counters[i], cnt[i]);
+                }
+            }
+        }
+    }
+
+    // ============================================================ insert ==
+    __device__ void do_insert(unsigned long long opi, const bh_op& o) {
+        const uint32_t n = o.len;
+        if (n == 0 || n > (uint32_t)K) {  // sort_batch capacity errors (batch.cpp:8-12)
+            status(opi, BH_E_CAPACITY, 0, ~0ull);
+            return;
+        }
+        Key* sorted = buf(0);
+        const Key* src = static_cast<const Key*>(rv.key_pool) + o.offset;
+        int bad = 0;
+        for (uint32_t i = threadIdx.x; i < (uint32_t)K; i += T) {
+            Key v = kMaxKey;
+            if (i < n) {
+                v = src[i];
+                bad |= v >= kMaxKey;
+            }
+            sorted[i] = v;
+        }
+        if (__syncthreads_or(bad)) {  // batch.cpp:13-15, before any mutation
+            status(opi, BH_E_INVALID_KEY, 0, ~0ull);
+            return;
+        }
+        cta_bitonic_sort<Key, K, T>(sorted);
+        rec(kEvInv, 0);
+
+        // ---- root phase (heap.cpp:126-167) ----
+        if (leader()) {
+            lead_lock_avail(1);
+            sh->nodes = ld_cg_u64(&hdr->node_count);
+            sh->plen = ld_cg_u64(&hdr->partial_len);
+        }
+        __syncthreads();
+        const unsigned long long nodes = sh->nodes;
+        const uint32_t plen = (uint32_t)sh->plen;
+        const bool full = n + plen >= (uint32_t)K;
+        if (full && nodes == hv.max_nodes) {  // heap.cpp:129-135
+            if (leader()) {
+                rec(kEvRel, 1);
+                lead_release_only(1, kAvail);
+            }
+            rec_abort();
+            status(opi, BH_E_CAPACITY, 0, ~0ull);
+            return;
+        }
+        unsigned long long seq = 0;
+        if (leader()) {
+            seq = ld_cg_u64(&hdr->root_seq);
+            st_cg_u64(&hdr->root_seq, seq + 1);
+        }
+        count(cInserts);
+        Key* part = buf(1);
+        Key* comb = buf(2);  // 2K wide: buf(2), buf(3)
+        if (plen) cta_load<Key, T>(part, partial, plen);
+        __syncthreads();
+        cta_merge<Key, T>(sorted, n, part, plen, comb, 2 * K, comb);
+        __syncthreads();
+        const uint32_t total = n + plen;
+
+        if (!full) {
+            if (nodes >= 1) {
+                Key* root = buf(4);
+                cta_load<Key, T>(root, node(1), K);
+                __syncthreads();
+                if (elide && comb[0] >= root[K - 1]) {
+                    count(cElided);
+                    cta_store<Key, T>(partial, comb, total);
+                } else {
+                    // merge_and_sort(root, combined): hi -> root, lo -> partial
+                    cta_merge<Key, T>(root, K, comb, total, node(1), K, partial);
+                    count(cMerges);
+                }
+            } else {
+                cta_store<Key, T>(partial, comb, total);
+            }
+            note_partial(total);
+            __syncthreads();
+            if (leader()) {
+                st_cg_u64(&hdr->partial_len, total);
+                lead_unlock(1);
+            }
+            status(opi, BH_OK, 0, seq);
+            rec(kEvRes, 0);
+            return;
+        }
+
+        if (total > (uint32_t)K) cta_store<Key, T>(partial, comb + K, total - K);
+        note_partial(total - K);
+        const unsigned long long rank = nodes + 1;
+        if (leader()) {
+            st_cg_u64(&hdr->partial_len, total - K);
+            st_cg_u64(&hdr->insert_count, ld_cg_u64(&hdr->insert_count) + 1);
+            st_cg_u64(&hdr->node_count, rank);
+        }
+        if (rank == 1) {
+            cta_store<Key, T>(node(1), comb, K);
+            count(cVisits);
+            __syncthreads();
+            if (leader()) lead_unlock(1);
+            status(opi, BH_OK, 0, seq);
+            rec(kEvRes, 0);
+            return;
+        }
+        const unsigned long long target = slot_for_rank(rank);
+        // The carried batch lives in comb[0,K) = buf(2); free: 0, 1, 4, 5.
+        if (hv.variant == BH_TD)
+            insert_td(target);
+        else
+            insert_bu(target);
+        status(opi, BH_OK, 0, seq);
+        rec(kEvRes, 0);
+    }
+
+    // merge_step_down (heap.cpp:190-205): node `slot` keeps the k smallest of
+    // node U batch; batch keeps the rest.  `bat` may be rotated with the free
+    // buffers nd/tmp.  Ends with a barrier.
+    __device__ void merge_step_down(Key*& bat, Key*& nd, Key*& tmp, unsigned long long slot) {
+        cta_load<Key, T>(nd, node(slot), K);
+        __syncthreads();
+        if (slot != 1 && nd[0] == kMaxKey && leader())
+            atomicOr(&hdr->error_flags, (unsigned long long)kErrInteriorEmpty);
+        if (elide && !needs_merge_full<Key, K>(nd, bat)) {
+            count(cElided);
+            if (!(nd[K - 1] <= bat[0])) {
+                cta_store<Key, T>(node(slot), bat, K);  // swap
+                Key* t = bat;
+                bat = nd;
+                nd = t;
+            }
+        } else {
+            cta_merge_full<Key, K, T>(nd, bat, node(slot), tmp);
+            count(cMerges);
+            Key* t = bat;
+            bat = tmp;
+            tmp = t;
+        }
+        __syncthreads();
+    }
+
+    // insert_td (heap.cpp:218-293).  Root held on entry.
+    __device__ void insert_td(unsigned long long target) {
+        Key* bat = buf(2);
+        Key* nd = buf(4);
+        Key* tmp = buf(5);
+        if (leader()) {  // claim the target under the root lock
+            uint32_t* p = st(target);
+            Backoff b;
+            for (;;) {
+                if (state_load(p) == kAvail && state_cas(p, kAvail, kTarget)) break;
+                b.pause();
+            }
+        }
+        merge_step_down(bat, nd, tmp, 1);
+        count(cVisits);
+        unsigned long long cur = 1;
+        const int depth = (int)level_of(target);
+        enum { kShip = 1, kWrite = 2, kSkip = 3, kMerge = 4 };
+        for (int lvl = depth - 1; lvl >= 0; --lvl) {
+            const unsigned long long next = target >> lvl;
+            if (leader()) {
+                uint32_t act = 0;
+                if (cur != 1 && state_load(st(target)) == kMarked) {
+                    act = kShip;
+                } else if (next == target) {
+                    Backoff b;
+                    for (;;) {
+                        const uint32_t s = state_load(st(target));
+                        if (s == kTarget) {
+                            if (state_cas(st(target), kTarget, kInUse)) {
+                                act = kWrite;
+                                break;
+                            }
+                        } else if (s == kMarked) {
+                            act = kShip;
+                            break;
+                        } else {
+                            b.pause();
+                        }
+                    }
+                } else {
+                    Backoff b;
+                    for (;;) {
+                        const uint32_t s = state_load(st(next));
+                        if (s == kAvail) {
+                            if (state_cas(st(next), kAvail, kInUse)) {
+                                act = kMerge;
+                                break;
+                            }
+                        } else if (s == kTarget || s == kMarked) {
+                            act = kSkip;  // frozen empty while we hold its ancestor
+                            break;
+                        } else {
+                            b.pause();
+                        }
+                    }
+                }
+                sh->act = act;
+            }
+            __syncthreads();
+            const uint32_t act = sh->act;
+            if (act == kShip) {  // ship_to_root (heap.cpp:207-216)
+                cta_store<Key, T>(node(1), bat, K);
+                count(cCoop);
+                __syncthreads();
+                if (leader()) {
+                    lead_release_only(target, kAvail);
+                    lead_unlock(cur);
+                }
+                return;
+            }
+            if (act == kWrite) {
+                if (leader()) {
+                    rec(kEvAcq, target);
+                    lead_unlock(cur);
+                }
+                cta_store<Key, T>(node(target), bat, K);
+                count(cVisits);
+                __syncthreads();
+                if (leader()) lead_unlock(target);
+                return;
+            }
+            if (act == kSkip) continue;
+            if (leader()) rec(kEvAcq, next);
+            merge_step_down(bat, nd, tmp, next);
+            count(cVisits);
+            if (leader()) lead_unlock(cur);
+            cur = next;
+        }
+    }
+
+    // abandon_park (heap.cpp:393-407).  Leader only.
+    __device__ void lead_abandon_park(unsigned long long slot) {
+        Backoff b;
+        for (;;) {
+            const uint32_t s = state_load(st(slot));
+            if (s == kDelMod) {
+                if (state_cas(st(slot), kDelMod, kAvail)) return;
+            } else if (s == kAvail || s == kInsHold) {
+                return;
+            } else {
+                b.pause();
+            }
+        }
+    }
+
+    // insert_bu (heap.cpp:295-373).  Root held on entry.
+    __device__ void insert_bu(unsigned long long target) {
+        Key* bat = buf(2);
+        Key* par = buf(4);
+        Key* cu = buf(5);
+        if (leader()) {
+            uint32_t* p = st(target);
+            Backoff b;
+            for (;;) {
+                const uint32_t s = state_load(p);
+                if (s == kAvail && state_cas(p, kAvail, kInUse)) break;
+                if (s == kDelMod && state_cas(p, kDelMod, kInUse)) break;
+                b.pause();
+            }
+            rec(kEvAcq, target);
+        }
+        cta_store<Key, T>(node(target), bat, K);
+        count(cVisits);
+        __syncthreads();
+        if (leader()) lead_unlock(1);
+
+        unsigned long long cur = target;  // held
+        while (cur != 1) {
+            const unsigned long long parent = cur >> 1;
+            if (leader()) {
+                // park: others may take the slot meanwhile
+                rec(kEvRel, cur);
+                lead_release_only(cur, kInsHold);
+                uint32_t* pp = st(parent);
+                Backoff b;
+                for (;;) {
+                    const uint32_t s = state_load(pp);
+                    if (s == kAvail && state_cas(pp, kAvail, kInUse)) break;
+                    if (s == kDelMod && state_cas(pp, kDelMod, kInUse)) break;
+                    b.pause();
+                }
+                rec(kEvAcq, parent);
+            }
+            __syncthreads();
+            cta_load<Key, T>(par, node(parent), K);
+            __syncthreads();
+            if (par[0] == kMaxKey) {
+                // parent was deleted: the subtree with our parked slot is gone
+                if (leader()) {
+                    lead_unlock(parent);
+                    lead_abandon_park(cur);
+                }
+                return;
+            }
+            if (leader()) {
+                uint32_t owned = 0;
+                uint32_t* pc = st(cur);
+                Backoff b;
+                for (;;) {
+                    const uint32_t s = state_load(pc);
+                    if (s == kInsHold) {
+                        if (state_cas(pc, kInsHold, kInUse)) {
+                            owned = 1;
+                            break;
+                        }
+                    } else if (s == kDelMod) {
+                        if (state_cas(pc, kDelMod, kAvail)) break;
+                    } else if (s == kAvail) {
+                        break;
+                    } else {
+                        b.pause();  // INUSE: a deleter is working on it
+                    }
+                }
+                if (owned) rec(kEvAcq, cur);
+                sh->owned = owned;
+            }
+            __syncthreads();
+            if (sh->owned) {
+                // The parked slot may have been consumed and re-claimed by a
+                // later insert (see heap.cpp:393-407), so re-read it.
+                cta_load<Key, T>(cu, node(cur), K);
+                __syncthreads();
+                if (cu[0] >= par[K - 1]) {
+                    count(cEarlyStops);
+                    if (leader()) {
+                        rec(kEvRel, cur);
+                        rec(kEvRel, parent);
+                        __threadfence();
+                        state_store_release(st(cur), kAvail);
+                        state_store_release(st(parent), kAvail);
+                    }
+                    return;
+                }
+                // merge_step_up (heap.cpp:375-391): parent keeps the k smallest
+                if (elide && !needs_merge_full<Key, K>(cu, par)) {
+                    count(cElided);
+                    cta_store<Key, T>(node(parent), cu, K);
+                    cta_store<Key, T>(node(cur), par, K);
+                } else {
+                    cta_merge_full<Key, K, T>(cu, par, node(parent), node(cur));
+                    count(cMerges);
+                }
+                count(cVisits);
+                __syncthreads();
+                if (leader()) lead_unlock(cur);
+            }
+            cur = parent;
+        }
+        if (leader()) lead_unlock(1);
+    }
+
+    // ============================================================ delete ==
+    __device__ void do_delete(unsigned long long opi, const bh_op& o) {
+        rec(kEvInv, 0);
+        if (leader()) {
+            lead_lock_avail(1);
+            sh->nodes = ld_cg_u64(&hdr->node_count);
+            sh->plen = ld_cg_u64(&hdr->partial_len);
+            const unsigned long long seq = ld_cg_u64(&hdr->root_seq);
+            st_cg_u64(&hdr->root_seq, seq + 1);
+            sh->seq = seq;
+        }
+        __syncthreads();
+        const unsigned long long nodes = sh->nodes;
+        const uint32_t plen = (uint32_t)sh->plen;
+        const unsigned long long seq = sh->seq;
+        Key* out = static_cast<Key*>(rv.out_pool) + o.offset;
+
+        if (nodes == 0) {
+            if (plen == 0) {  // empty heap (heap.cpp:424-429)
+                if (leader()) lead_unlock(1);
+                status(opi, BH_E_EMPTY, 0, seq);
+                rec(kEvRes, 0);
+                return;
+            }
+            // fewer than k keys: they all live in the partial buffer
+            cta_copy_gg<Key, T>(out, partial, plen);
+            count(cDeletes);
+            __syncthreads();
+            if (leader()) {
+                st_cg_u64(&hdr->partial_len, 0);
+                st_cg_u64(&hdr->delete_count, ld_cg_u64(&hdr->delete_count) + 1);
+                lead_unlock(1);
+            }
+            status(opi, BH_OK, plen, seq);
+            rec(kEvRes, 0);
+            return;
+        }
+
+        int ci = 0;  // buffer index holding the carried (cur) batch
+        Key* cur_s = buf(ci);
+        cta_load<Key, T>(cur_s, node(1), K);
+        __syncthreads();
+        cta_store<Key, T>(out, cur_s, K);
+        if (leader() && cur_s[K - 1] == kMaxKey)
+            atomicOr(&hdr->error_flags, (unsigned long long)kErrSentinelEscaped);
+        count(cDeletes);
+        if (leader()) {
+            st_cg_u64(&hdr->delete_count, ld_cg_u64(&hdr->delete_count) + 1);
+            st_cg_u64(&hdr->node_count, nodes - 1);
+        }
+        if (nodes == 1) {
+            cta_fill<Key, T>(node(1), kMaxKey, K);
+            __syncthreads();
+            if (leader()) lead_unlock(1);
+            status(opi, BH_OK, K, seq);
+            rec(kEvRes, 0);
+            return;
+        }
+
+        // ---- refill_root_from(last) (heap.cpp:467-531) ----
+        const unsigned long long last = slot_for_rank(nodes);
+        enum { kTake = 1, kCoop = 2 };
+        if (leader()) {
+            uint32_t* p = st(last);
+            uint32_t act = 0, rel = kAvail;
+            Backoff b;
+            for (;;) {
+                const uint32_t s = state_load(p);
+                if (s == kAvail) {
+                    if (state_cas(p, kAvail, kInUse)) {
+                        act = kTake;
+                        break;
+                    }
+                } else if (hv.variant == BH_TD && s == kTarget) {
+                    if (state_cas(p, kTarget, kMarked)) {
+                        act = kCoop;
+                        break;
+                    }
+                } else if (hv.variant == BH_BU && s == kInsHold) {
+                    if (state_cas(p, kInsHold, kInUse)) {  // take the in-flight batch
+                        act = kTake;
+                        rel = kDelMod;
+                        break;
+                    }
+                } else if (hv.variant == BH_BU && s == kDelMod) {
+                    if (state_cas(p, kDelMod, kInUse)) {
+                        act = kTake;
+                        break;
+                    }
+                } else {
+                    b.pause();
+                }
+            }
+            if (act == kCoop) {
+                // the inserter ships its batch into the root, then AVAIL
+                Backoff w;
+                while (state_load(p) != kAvail) w.pause();
+            } else {
+                rec(kEvAcq, last);
+            }
+            sh->act = act;
+            sh->lrel = rel;
+        }
+        __syncthreads();
+        if (sh->act == kTake) {
+            cta_load<Key, T>(cur_s, node(last), K);
+            __syncthreads();
+            cta_fill<Key, T>(node(last), kMaxKey, K);
+            __syncthreads();
+            if (leader()) lead_unlock(last, sh->lrel);
+        } else {
+            cta_load<Key, T>(cur_s, node(1), K);
+            __syncthreads();
+        }
+
+        // ---- remerge_root_with_partial (heap.cpp:533-545) ----
+        if (plen) {
+            Key* sp = buf(1);
+            Key* tmp = buf(2);
+            cta_load<Key, T>(sp, partial, plen);
+            __syncthreads();
+            if (elide && sp[0] >= cur_s[K - 1]) {
+                count(cElided);
+            } else {
+                cta_merge<Key, T>(cur_s, K, sp, plen, tmp, K, partial);
+                count(cMerges);
+                note_partial(plen);
+                ci = 2;
+                cur_s = tmp;
+            }
+            __syncthreads();
+        }
+        heapify_down(ci);
+        status(opi, BH_OK, K, seq);
+        rec(kEvRes, 0);
+    }
+
+    // acquire_child (heap.cpp:547-585).  Leader only.  Returns locked?;
+    // rel = state to release with.
+    __device__ uint32_t lead_acquire_child(unsigned long long slot, uint32_t& rel) {
+        rel = kAvail;
+        if (slot > hv.slot_count) return 0;
+        uint32_t* p = st(slot);
+        Backoff b;
+        for (;;) {
+            const uint32_t s = state_load(p);
+            if (s == kAvail) {
+                if (state_cas(p, kAvail, kInUse)) break;
+            } else if (hv.variant == BH_TD && (s == kTarget || s == kMarked)) {
+                return 0;  // frozen empty while we hold the parent
+            } else if (hv.variant == BH_BU && s == kInsHold) {
+                if (state_cas(p, kInsHold, kInUse)) {
+                    rel = kDelMod;
+                    break;
+                }
+            } else if (hv.variant == BH_BU && s == kDelMod) {
+                if (state_cas(p, kDelMod, kInUse)) break;
+            } else {
+                b.pause();
+            }
+        }
+        rec(kEvAcq, slot);
+        return 1;
+    }
+
+    // heapify_down (heap.cpp:591-667) with the carried batch in buf(ci).
+    // Root held on entry; all held locks are released on exit.
+    __device__ void heapify_down(int ci) {
+        unsigned long long cur = 1;
+        uint32_t cur_rel = kAvail;
+        for (;;) {
+            Key* cur_s = buf(ci);
+            Key* L = buf((ci + 1) % kBufs);
+            Key* R = buf((ci + 2) % kBufs);
+            Key* H = buf((ci + 3) % kBufs);
+            Key* nx = buf((ci + 4) % kBufs);
+            const unsigned long long l = 2 * cur, r = 2 * cur + 1;
+            if (leader()) {
+                uint32_t lrel, rrel;
+                sh->lk = lead_acquire_child(l, lrel);
+                sh->rk = lead_acquire_child(r, rrel);
+                sh->lrel = lrel;
+                sh->rrel = rrel;
+            }
+            __syncthreads();
+            const uint32_t lk = sh->lk, rk = sh->rk;
+            if (lk) cta_load<Key, T>(L, node(l), K);
+            if (rk) cta_load<Key, T>(R, node(r), K);
+            __syncthreads();
+            const bool lempty = !lk || L[0] == kMaxKey;
+            const bool rempty = !rk || R[0] == kMaxKey;
+            const Key cmax = cur_s[K - 1];
+            bool stop = lempty && rempty;
+            if (!stop) {
+                const Key lmin = lempty ? kMaxKey : L[0];
+                const Key rmin = rempty ? kMaxKey : R[0];
+                if (cmax <= lmin && cmax <= rmin) {
+                    count(cEarlyStops);
+                    stop = true;
+                }
+            }
+            if (stop) {
+                cta_store<Key, T>(node(cur), cur_s, K);
+                __syncthreads();
+                if (leader()) {
+                    if (lk) rec(kEvRel, l);
+                    if (rk) rec(kEvRel, r);
+                    rec(kEvRel, cur);
+                    __threadfence();
+                    if (lk) state_store_release(st(l), sh->lrel);
+                    if (rk) state_store_release(st(r), sh->rrel);
+                    state_store_release(st(cur), cur_rel);
+                }
+                return;
+            }
+            // Merge the children: lo lands in the child whose max was larger
+            // (right on ties), hi in the other, which we descend into.
+            bool hi_left;
+            Key* hdata;
+            int hidx;
+            if (lempty) {
+                hi_left = false;
+                hdata = R;
+                hidx = (ci + 2) % kBufs;
+            } else if (rempty) {
+                hi_left = true;
+                hdata = L;
+                hidx = (ci + 1) % kBufs;
+            } else if (elide && !needs_merge_full<Key, K>(L, R)) {
+                count(cElided);
+                // fix of heap.cpp:628-636: the batch with the smaller keys is hi
+                hi_left = L[K - 1] <= R[0];
+                hdata = hi_left ? L : R;
+                hidx = hi_left ? (ci + 1) % kBufs : (ci + 2) % kBufs;
+            } else {
+                hi_left = !(L[K - 1] > R[K - 1]);
+                cta_merge_full<Key, K, T>(L, R, H, node(hi_left ? r : l));
+                count(cMerges);
+                __syncthreads();
+                hdata = H;
+                hidx = (ci + 3) % kBufs;
+            }
+            const unsigned long long hi = hi_left ? l : r;
+            const unsigned long long lo = hi_left ? r : l;
+            const uint32_t lo_locked = hi_left ? rk : lk;
+            int next_ci;
+            if (elide && !needs_merge_full<Key, K>(cur_s, hdata)) {
+                // early stop ruled out the ordered case: a full inversion
+                count(cElided);
+                cta_store<Key, T>(node(cur), hdata, K);
+                next_ci = ci;  // old cur batch moves down into hi
+            } else {
+                cta_merge_full<Key, K, T>(cur_s, hdata, node(cur), nx);
+                count(cMerges);
+                next_ci = (ci + 4) % kBufs;
+            }
+            (void)hidx;
+            count(cVisits);
+            __syncthreads();
+            const uint32_t hi_rel = hi_left ? sh->lrel : sh->rrel;
+            if (leader()) {
+                const uint32_t lo_rel = hi_left ? sh->rrel : sh->lrel;
+                if (lo_locked) rec(kEvRel, lo);
+                rec(kEvRel, cur);
+                __threadfence();
+                if (lo_locked) state_store_release(st(lo), lo_rel);
+                state_store_release(st(cur), cur_rel);
+            }
+            cur = hi;
+            cur_rel = hi_rel;
+            ci = next_ci;
+            __syncthreads();  // sh->lrel/rrel reused next level
+        }
+    }
+};
+
+template <typename Key, int K, int T>
+__global__ void __launch_bounds__(T) heap_ops_kernel(HeapView hv, RunView rv) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ OpShared sh;
+    HeapCta<Key, K, T> cta(hv, rv, smem_raw, &sh);
+    cta.run();
+}
+
+template <typename Key, int K>
+struct KernelCfg {
+    static constexpr int kThreads = K / 2 < 32 ? 32 : (K / 2 > 512 ? 512 : K / 2);
+    static constexpr uint32_t kSmem = 6u * K * sizeof(Key);
+};
+
+}  // namespace bh

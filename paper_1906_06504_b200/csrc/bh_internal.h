@@ -1,0 +1,118 @@
+// bh_internal.h -- layouts shared by the host C ABI and the device kernels.
+#pragma once
+
+#include <cstdint>
+
+#include "batchheap_b200.h"
+
+namespace bh {
+
+// Node state words (reference proj/include/batchheap/heap.hpp:107-114).
+enum : uint32_t {
+    kAvail = 0,
+    kInUse = 1,
+    kTarget = 2,
+    kMarked = 3,
+    kInsHold = 4,
+    kDelMod = 5,
+};
+
+// One state word per 32-byte sector so lock traffic on neighbouring nodes
+// never shares an L2 atomic sector.
+constexpr uint32_t kStateStride = 8;  // uint32 words
+
+// Heap header, root-lock guarded (reference heap.hpp:173-177).  One cache
+// line; the partial buffer follows in its own allocation.
+struct alignas(128) Header {
+    unsigned long long node_count;
+    unsigned long long insert_count;
+    unsigned long long delete_count;  // root-lock sequence of deletes
+    unsigned long long root_seq;      // root-lock sequence of all ops
+    unsigned long long partial_len;
+    unsigned long long error_flags;   // protocol faults seen on device
+    unsigned long long clock;         // event-log clock (RECORD)
+    unsigned long long pad;
+};
+
+// Device counters (reference HeapCounters, heap.hpp:49-58).
+enum CounterIdx {
+    cInserts = 0,
+    cDeletes,
+    cMerges,
+    cElided,
+    cEarlyStops,
+    cVisits,
+    cCoop,
+    cMaxPartial,
+    kNumCounters
+};
+
+enum ErrorFlag : unsigned long long {
+    kErrSentinelEscaped = 1ull << 0,  // heap.cpp:462-463
+    kErrInteriorEmpty = 1ull << 1,    // heap.cpp:286 assert
+    kErrEventOverflow = 1ull << 2,
+};
+
+enum EventKind : uint16_t { kEvInv = 0, kEvRes = 1, kEvAcq = 2, kEvRel = 3 };
+
+struct DevEvent {
+    unsigned long long ts;
+    uint32_t op;
+    uint16_t kind;
+    uint16_t pad;
+    unsigned long long node;
+};
+
+// Everything a kernel needs about one heap (by value as a kernel param).
+struct HeapView {
+    void* keys;              // slot_count * k keys; node i (1-based) at (i-1)*k
+    uint32_t* states;        // (slot_count + 1) * kStateStride
+    Header* hdr;
+    void* partial;           // k keys
+    unsigned long long* counters;
+    unsigned long long slot_count;
+    uint32_t k;
+    uint32_t max_nodes;
+    uint32_t variant;
+    uint32_t flags;
+};
+
+struct RunView {
+    const bh_op* ops;
+    unsigned long long n_ops;
+    const void* key_pool;
+    void* out_pool;
+    uint32_t* out_status;
+    uint32_t* out_lens;
+    unsigned long long* out_seq;
+    unsigned long long* ticket;
+    DevEvent* events;        // n_ops * ev_per_op (RECORD only)
+    uint32_t* event_counts;  // n_ops
+    uint32_t ev_per_op;
+};
+
+// Kernel launch table entry (one per key width x k).
+struct KernelInfo {
+    uint32_t threads;
+    uint32_t smem_bytes;
+    int max_ctas_per_sm;
+};
+
+}  // namespace bh
+
+// Device-side dispatch implemented in bh_kernels_*.cu.
+extern "C" int bh_internal_launch_ops(uint32_t key_bits, const bh::HeapView* hv, const bh::RunView* rv,
+                                      uint32_t ctas, void* stream);
+extern "C" int bh_internal_kernel_info(uint32_t key_bits, uint32_t k, bh::KernelInfo* info);
+extern "C" int bh_internal_launch_sort(uint32_t key_bits, uint32_t k, void* keys, const uint32_t* lens,
+                                       uint64_t batches, void* stream);
+extern "C" int bh_internal_launch_merge(uint32_t key_bits, uint32_t k, const void* a, const void* b,
+                                        void* hi, void* lo, uint64_t pairs, void* stream);
+extern "C" int bh_internal_launch_check(uint32_t key_bits, const bh::HeapView* hv,
+                                        unsigned long long* result /* device, 4 words */,
+                                        void* stream);
+extern "C" int bh_internal_launch_gather(uint32_t key_bits, const bh::HeapView* hv,
+                                         unsigned long long nodes, void* out /* device */,
+                                         void* stream);
+extern "C" int bh_internal_launch_plan(int kind, uint32_t k, uint64_t n_keys, bh_op* ops,
+                                       void* stream);

@@ -1,0 +1,53 @@
+"""Quick phase-separated timing probe (not the bench): insert-all then
+delete-all of n u32 keys at node capacity k, device-resident inputs."""
+import argparse
+import sys
+import os
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_1906_06504_b200 import GeneralizedHeap, Variant, generate_keys, phase_ops
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--log2n", type=int, default=26)
+ap.add_argument("--k", type=int, nargs="+", default=[1024])
+ap.add_argument("--variant", default="bu")
+ap.add_argument("--ctas", type=int, nargs="+", default=[0])
+ap.add_argument("--reps", type=int, default=1)
+a = ap.parse_args()
+n = 1 << a.log2n
+dev = torch.device("cuda")
+keys = generate_keys(n, 1, key_bits=32)
+pool = torch.from_numpy(keys.view(np.int32)).to(dev)
+for k in a.k:
+    for ctas in a.ctas:
+        for rep in range(a.reps):
+            heap = GeneralizedHeap(Variant.BU if a.variant == "bu" else Variant.TD, k, n // k + 1024, key_bits=32)
+            n_ops = n // k
+            ops_i = torch.from_numpy(phase_ops(0, n, k).view(np.uint8)).to(dev)
+            ops_d = torch.from_numpy(phase_ops(1, n, k).view(np.uint8)).to(dev)
+            out = torch.empty(n, dtype=torch.int32, device=dev)
+            st = torch.zeros(n_ops, dtype=torch.int32, device=dev)
+            seq = torch.empty(n_ops, dtype=torch.int64, device=dev)
+            s = torch.cuda.current_stream()
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            torch.cuda.synchronize()
+            e0.record(s)
+            heap.run_ops_ptr(ops_i.data_ptr(), n_ops, pool.data_ptr(), 0, st.data_ptr(), 0, 0, ctas=ctas, stream=s.cuda_stream)
+            e1.record(s)
+            heap.run_ops_ptr(ops_d.data_ptr(), n_ops, 0, out.data_ptr(), st.data_ptr(), 0, seq.data_ptr(), ctas=ctas, stream=s.cuda_stream)
+            e2.record(s)
+            torch.cuda.synchronize()
+            ti, td = e0.elapsed_time(e1), e1.elapsed_time(e2)
+            order = torch.argsort(seq)
+            stream = out.view(n_ops, k)[order].reshape(-1)
+            ok = bool((stream[:-1].to(torch.int64) & 0xFFFFFFFF).le(stream[1:].to(torch.int64) & 0xFFFFFFFF).all())
+            c = heap.counters()
+            print(f"k={k} ctas={ctas or heap.max_ctas} n=2^{a.log2n} {a.variant}: insert {ti:.2f} ms "
+                  f"delete {td:.2f} ms  key-ops/s {2*n/((ti+td)/1e3):.3e} sorted={ok} "
+                  f"merges={c.merges} elided={c.elided_merges} early={c.early_stops} visits={c.propagation_node_visits}",
+                  flush=True)
+            heap.close()
