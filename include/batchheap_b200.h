@@ -49,6 +49,7 @@ enum { BH_TD = 0, BH_BU = 1 };
 /* bh_create flags. */
 #define BH_FLAG_ELIDE_MERGES 0x1u /* HeapOptions::elide_merges (heap.hpp:43-47); default on */
 #define BH_FLAG_RECORD 0x2u       /* device event log for linearizability checks (Recorder*) */
+#define BH_FLAG_PROFILE 0x4u      /* per-phase SM-cycle counters (bh_profile) */
 
 typedef struct bh_heap bh_heap;
 
@@ -80,11 +81,12 @@ typedef struct {
     uint64_t offset; /* insert: first key in key_pool; delete: first slot (k wide) in out_pool */
 } bh_op;
 
-/* Per-op status written by a bulk run (same codes as above). */
+/* Launch configuration of a bulk run. */
+#define BH_RUN_EXPLICIT_STREAM 0x1u /* use cfg->stream even when NULL (legacy default stream) */
 typedef struct {
     uint32_t ctas;   /* persistent CTAs; 0 = all co-resident CTAs the device holds */
-    uint32_t flags;  /* reserved, 0 */
-    void* stream;    /* cudaStream_t for bh_run_ops_device; NULL = the handle's stream */
+    uint32_t flags;  /* BH_RUN_* */
+    void* stream;    /* cudaStream_t; NULL = the handle's own stream unless BH_RUN_EXPLICIT_STREAM */
 } bh_run_cfg;
 
 /* ---------------------------------------------------------------------------
@@ -171,6 +173,15 @@ typedef struct {
     uint64_t node;
 } bh_event;
 BH_API int bh_history(bh_heap* heap, bh_event* out, uint64_t cap, uint64_t* n_out);
+
+/* Cycle profile of BH_FLAG_PROFILE handles (no reference analogue; the
+ * reference's only timing is wall clock around whole runs).  Fills up to
+ * `cap` words: [0] insert ops, [1] sort cycles, [2] root-wait cycles,
+ * [3] root-hold cycles, [4] post-root cycles, [5] delete ops, [6] delete
+ * root-wait, [7] delete root-hold, [8] delete heapify cycles, [9] child-lock
+ * wait cycles, [10] heapify levels, [11] CTA busy cycles.  reset != 0 zeroes
+ * the counters after reading. */
+BH_API int bh_profile(bh_heap* heap, uint64_t* out, uint32_t cap, int reset);
 
 /* Thread-local message for the last failing call on this thread. */
 BH_API const char* bh_last_error(void);

@@ -150,6 +150,81 @@ def check_bu(history: List[OpRecord], k: int) -> CheckResult:
     return replay_in_order(sorted(history, key=key), k)
 
 
+def real_time_violation(witness: List[OpRecord]) -> Optional[str]:
+    """A witness must keep real-time order: if b responded before a was
+    invoked, b precedes a (section 2.3).  Returns why not, or None."""
+    n = len(witness)
+    suffix = [None] * (n + 1)  # (min respond_ts, index) over witness[i:]
+    best = None
+    for i in range(n - 1, -1, -1):
+        r = witness[i].respond_ts
+        if best is None or r < best[0]:
+            best = (r, i)
+        suffix[i] = best
+    for i in range(n - 1):
+        ts, j = suffix[i + 1]
+        if ts < witness[i].invoke_ts:
+            return (f"{_describe(witness[j])} responded before {_describe(witness[i])} was invoked "
+                    f"but is ordered after it")
+    return None
+
+
+def check_bu_repaired(history: List[OpRecord], k: int) -> CheckResult:
+    """check_bu, extended for one interleaving the constructive order cannot
+    place: a deleter that refills the root from (or heapifies through) a
+    parked BU insert's slot (INSHOLD -> DELMOD, proj/src/heap.cpp:508-516,
+    :567-573) makes that insert's keys deletable before the insert's last
+    lock release.  When a delete returns keys the reL order has not inserted
+    yet, the inserts that carry them and were invoked before the delete's
+    root release are moved to just before it.  The result is PASS only with a
+    witness that respects real-time order and replays exactly through the
+    multiset oracle, so PASS still proves linearizability."""
+    def key(o):
+        return (o.last_release_ts if o.op == INSERT else o.root_release_ts, o.worker)
+    ordered = sorted(history, key=key)
+    applied = set()
+    witness: List[OpRecord] = []
+    state = SortedList()
+    moved = 0
+    for idx, op in enumerate(ordered):
+        if op.opid in applied:
+            continue
+        if op.op == INSERT:
+            state.update(op.keys)
+            applied.add(op.opid)
+            witness.append(op)
+            continue
+        want = list(op.keys)
+        take = min(k, len(state))
+        if list(state[:take]) != want:
+            wanted = set(want)
+            for cand in ordered[idx + 1:]:
+                if cand.op != INSERT or cand.opid in applied:
+                    continue
+                if cand.invoke_ts >= op.root_release_ts or not (wanted & set(cand.keys)):
+                    continue
+                state.update(cand.keys)
+                applied.add(cand.opid)
+                witness.append(cand)
+                moved += 1
+                take = min(k, len(state))
+                if list(state[:take]) == want:
+                    break
+        take = min(k, len(state))
+        got = [state.pop(0) for _ in range(take)]
+        if got != want:
+            return CheckResult(False, f"{_describe(op)} returned {want[:4]} but the oracle gives {got[:4]}")
+        applied.add(op.opid)
+        witness.append(op)
+    bad = real_time_violation(witness)
+    if bad:
+        return CheckResult(False, "repaired witness breaks real-time order: " + bad)
+    res = replay_in_order(witness, k)
+    if res.passed:
+        res.detail = f"moved {moved} inserts"
+    return res
+
+
 def check_exhaustive(history: List[OpRecord], k: int) -> CheckResult:
     n = len(history)
     if n > 20:

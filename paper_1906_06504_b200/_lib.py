@@ -18,7 +18,9 @@ BH_OK, BH_E_CONFIG, BH_E_CAPACITY, BH_E_EMPTY, BH_E_INVALID_KEY, BH_E_CUDA, BH_E
 BH_TD, BH_BU = 0, 1
 BH_FLAG_ELIDE_MERGES = 0x1
 BH_FLAG_RECORD = 0x2
+BH_FLAG_PROFILE = 0x4
 BH_OP_INSERT, BH_OP_DELETE = 0, 1
+BH_RUN_EXPLICIT_STREAM = 0x1
 
 
 class bh_peek(C.Structure):
@@ -67,6 +69,7 @@ SIGNATURES = {
     "bh_info": (_i, [_vp, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u64), C.POINTER(_u32),
                      C.POINTER(_i), C.POINTER(_u32), C.POINTER(_u32)]),
     "bh_history": (_i, [_vp, _vp, _u64, C.POINTER(_u64)]),
+    "bh_profile": (_i, [_vp, C.POINTER(_u64), _u32, _i]),
     "bh_last_error": (C.c_char_p, []),
     "bh_sort_batches": (_i, [_u32, _u32, _vp, _vp, _u64, _vp]),
     "bh_merge_split": (_i, [_u32, _u32, _vp, _vp, _vp, _vp, _u64, _vp]),

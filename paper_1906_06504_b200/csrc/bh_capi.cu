@@ -31,6 +31,13 @@ int check_u64(const HeapView&, unsigned long long*, cudaStream_t);
 int gather_u32(const HeapView&, unsigned long long, void*, cudaStream_t);
 int gather_u64(const HeapView&, unsigned long long, void*, cudaStream_t);
 
+thread_local cudaError_t g_last_cuda = cudaSuccess;
+int note_cuda(cudaError_t e) {
+    if (e == cudaSuccess) return BH_OK;
+    g_last_cuda = e;
+    return BH_E_CUDA;
+}
+
 __global__ void plan_kernel(int kind, uint32_t k, unsigned long long n_keys, unsigned long long n_ops,
                             bh_op* ops) {
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n_ops;
@@ -100,6 +107,7 @@ struct bh_heap {
     Header* d_hdr = nullptr;
     void* d_partial = nullptr;
     unsigned long long* d_counters = nullptr;
+    unsigned long long* d_prof = nullptr;
     unsigned long long* d_tickets = nullptr;  // ring of bulk tickets
     std::atomic<uint32_t> ticket_next{0};
     cudaStream_t stream = nullptr;
@@ -131,6 +139,7 @@ struct bh_heap {
         v.hdr = d_hdr;
         v.partial = d_partial;
         v.counters = d_counters;
+        v.prof = d_prof;
         v.slot_count = slot_count;
         v.k = k;
         v.max_nodes = max_nodes;
@@ -148,8 +157,16 @@ int launch_ops(bh_heap* h, const RunView& rv, uint32_t ctas, cudaStream_t s) {
     HeapView hv = h->view();
     int rc = h->key_bits == 32 ? ops_u32(hv, rv, ctas, s) : ops_u64(hv, rv, ctas, s);
     if (rc != BH_OK) return fail(rc, std::string("heap kernel launch failed: ") +
-                                         cudaGetErrorString(cudaGetLastError()));
+                                         cudaGetErrorString(g_last_cuda));
     return BH_OK;
+}
+
+// cfg->stream, or the handle's stream when cfg->stream is NULL and the
+// caller did not ask for the legacy default stream explicitly.
+cudaStream_t run_stream(bh_heap* h, const bh_run_cfg* cfg) {
+    if (cfg && (cfg->stream || (cfg->flags & BH_RUN_EXPLICIT_STREAM)))
+        return static_cast<cudaStream_t>(cfg->stream);
+    return h->stream;
 }
 
 uint32_t pick_ctas(bh_heap* h, uint64_t n_ops, const bh_run_cfg* cfg) {
@@ -360,6 +377,10 @@ int bh_create(bh_heap** out, int variant, uint32_t k, uint32_t max_nodes, uint32
     cudaMemsetAsync(h->d_hdr, 0, sizeof(Header), h->stream);
     cudaMemsetAsync(h->d_partial, 0xFF, std::max<size_t>((size_t)k * h->key_size, 16), h->stream);
     cudaMemsetAsync(h->d_counters, 0, kNumCounters * 8, h->stream);
+    if (flags & BH_FLAG_PROFILE) {
+        if ((e = cudaMalloc(&h->d_prof, 32 * 8)) != cudaSuccess) return cleanup(cuda_fail(e, "prof"));
+        cudaMemsetAsync(h->d_prof, 0, 32 * 8, h->stream);
+    }
     if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) return cleanup(cuda_fail(e, "init"));
     int rc = key_bits == 32 ? info_u32(k, &h->kinfo) : info_u64(k, &h->kinfo);
     if (rc != BH_OK) return cleanup(fail(rc, "kernel occupancy query failed"));
@@ -387,6 +408,7 @@ void bh_destroy(bh_heap* h) {
     cudaFree(h->d_hdr);
     cudaFree(h->d_partial);
     cudaFree(h->d_counters);
+    cudaFree(h->d_prof);
     cudaFree(h->d_tickets);
     cudaFree(h->d_stage);
     cudaFree(h->d_events);
@@ -417,7 +439,7 @@ int bh_run_ops_device(bh_heap* h, const bh_op* ops, uint64_t n_ops, const void* 
                       uint32_t* out_status, uint32_t* out_lens, uint64_t* out_seq, const bh_run_cfg* cfg) {
     if (!h) return fail(BH_E_CONFIG, "null heap");
     if (n_ops == 0) return BH_OK;
-    cudaStream_t s = (cfg && cfg->stream) ? static_cast<cudaStream_t>(cfg->stream) : h->stream;
+    cudaStream_t s = run_stream(h, cfg);
     BH_CUDA(cudaSetDevice(h->device));
     RunView rv{};
     rv.ops = ops;
@@ -458,7 +480,7 @@ int bh_run_ops(bh_heap* h, const bh_op* ops, uint64_t n_ops, const void* key_poo
     }
     std::lock_guard<std::mutex> g(h->bulk_mu);
     BH_CUDA(cudaSetDevice(h->device));
-    cudaStream_t s = (cfg && cfg->stream) ? static_cast<cudaStream_t>(cfg->stream) : h->stream;
+    cudaStream_t s = run_stream(h, cfg);
     auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t ops_b = align(n_ops * sizeof(bh_op));
     const size_t pool_b = align(std::max<uint64_t>(key_pool_len, 1) * h->key_size);
@@ -484,6 +506,7 @@ int bh_run_ops(bh_heap* h, const bh_op* ops, uint64_t n_ops, const void* key_poo
         BH_CUDA(cudaMemcpyAsync(d_pool, key_pool, key_pool_len * h->key_size, cudaMemcpyHostToDevice, s));
     bh_run_cfg c2 = cfg ? *cfg : bh_run_cfg{0, 0, nullptr};
     c2.stream = s;
+    c2.flags |= BH_RUN_EXPLICIT_STREAM;
     int rc = bh_run_ops_device(h, d_ops, n_ops, d_pool, d_out, d_status, d_lens, d_seq, &c2);
     if (rc != BH_OK) return rc;
     if (out_pool && out_pool_len)
@@ -710,6 +733,21 @@ int bh_history(bh_heap* h, bh_event* out, uint64_t cap, uint64_t* n_out) {
             out[at].node = d.node;
             ++at;
         }
+    return BH_OK;
+}
+
+int bh_profile(bh_heap* h, uint64_t* out, uint32_t cap, int reset) {
+    if (!h || !out) return fail(BH_E_CONFIG, "null argument");
+    if (!h->d_prof) return fail(BH_E_CONFIG, "heap was not created with BH_FLAG_PROFILE");
+    BH_CUDA(cudaSetDevice(h->device));
+    uint64_t buf[32];
+    BH_CUDA(cudaMemcpyAsync(buf, h->d_prof, sizeof(buf), cudaMemcpyDeviceToHost, h->aux));
+    BH_CUDA(cudaStreamSynchronize(h->aux));
+    std::memcpy(out, buf, std::min<uint32_t>(cap, 32) * 8);
+    if (reset) {
+        BH_CUDA(cudaMemsetAsync(h->d_prof, 0, sizeof(buf), h->aux));
+        BH_CUDA(cudaStreamSynchronize(h->aux));
+    }
     return BH_OK;
 }
 

@@ -50,11 +50,13 @@ __device__ __forceinline__ void state_store_release(uint32_t* p, uint32_t v) {
 // Spin backoff (reference Backoff, proj/src/heap.cpp:18-31: 2^0..2^5 pause
 // rounds, then yield).  On the GPU a waiting CTA sleeps in growing steps so the
 // lock holder's SM and the contended L2 slice stay free.
+// The first polls spin without sleeping: a lock hand-off on the critical
+// path should cost one L2 round trip, not a sleep quantum.
 struct Backoff {
-    uint32_t ns = 0;
+    uint32_t n = 0;
     __device__ __forceinline__ void pause() {
-        ns = ns == 0 ? 20 : (ns < 320 ? ns * 2 : ns);
-        __nanosleep(ns);
+        ++n;
+        if (n > 32) __nanosleep(n > 64 ? 256 : 64);
     }
 };
 

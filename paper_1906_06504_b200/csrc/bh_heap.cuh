@@ -12,13 +12,20 @@
 //   do_delete   heap.cpp:420-465   root take, refill (:467-531), partial
 //                                  re-merge (:533-545), heapify (:547-667)
 //
-// B200-specific choices (not in the reference):
-//   * node data moves through shared memory; the node a walk carries stays in
-//     shared memory and is written back once, when its lock is released;
-//   * the delete's root refill is kept in shared memory until the first
-//     heapify level releases the root (no one else reads the root meanwhile);
-//   * lock words are spun on by one elected thread (ld.acquire + CAS) with
-//     __nanosleep backoff; the outcome is broadcast with one barrier;
+// The throughput of a lock-based heap is set by how long each op holds the
+// root (and, for deletes, each level) -- a chain of dependent L2 round trips,
+// not bandwidth.  B200-specific choices that shorten those chains (none change
+// the protocol's states, transitions or lock order):
+//   * header words and the root batch are read in the same round trip;
+//   * a node's two children are claimed by two lanes at once;
+//   * the delete's root refill claims children 2 and 3 first and then the
+//     last node (ancestor-before-descendant, as everywhere else), so the refill
+//     and the first heapify level share their load round trip;
+//   * the carried batch stays in shared memory and is written back once, when
+//     its lock is released; the BU target is written after the root release
+//     (the target is already INUSE);
+//   * locks are released by one st.release.gpu after a CTA barrier (the
+//     barrier orders every thread's stores before the release);
 //   * counters are per-CTA registers folded into global memory at exit.
 //
 // Deliberate deviation: heapify's merge elision places the batch that holds
@@ -36,9 +43,27 @@ struct OpShared {
     unsigned long long plen;
     unsigned long long seq;
     uint32_t act;
-    uint32_t lk, rk;        // children locked?
-    uint32_t lrel, rrel;    // children release states
+    uint32_t lk, rk;      // children locked?
+    uint32_t lrel, rrel;  // children release states
+    uint32_t lastrel;
     uint32_t owned;
+};
+
+// Profile slots (BH_FLAG_PROFILE): SM cycles summed over ops by the leader.
+enum ProfIdx {
+    pfInsOps = 0,
+    pfInsSort,
+    pfInsRootWait,
+    pfInsRootHold,
+    pfInsRest,
+    pfDelOps,
+    pfDelRootWait,
+    pfDelRootHold,
+    pfDelRest,
+    pfChildWait,
+    pfLevels,
+    pfCtaCycles,
+    kNumProf
 };
 
 template <typename Key, int K, int T>
@@ -55,9 +80,11 @@ struct HeapCta {
     OpShared* sh;
     Key* bufs;
     unsigned long long cnt[kNumCounters];
+    unsigned long long pf[kNumProf];
     unsigned long long cur_op;
     bool elide;
     bool record;
+    bool prof;
 
     __device__ __forceinline__ HeapCta(const HeapView& h, const RunView& r, unsigned char* smem,
                                        OpShared* s)
@@ -69,8 +96,11 @@ struct HeapCta {
         bufs = reinterpret_cast<Key*>(smem);
 #pragma unroll
         for (int i = 0; i < kNumCounters; ++i) cnt[i] = 0;
+#pragma unroll
+        for (int i = 0; i < kNumProf; ++i) pf[i] = 0;
         elide = (h.flags & BH_FLAG_ELIDE_MERGES) != 0;
         record = (h.flags & BH_FLAG_RECORD) != 0;
+        prof = h.prof != nullptr;
     }
 
     __device__ __forceinline__ Key* buf(int i) const { return bufs + i * K; }
@@ -82,14 +112,19 @@ struct HeapCta {
     __device__ __forceinline__ void count(int idx, unsigned long long v = 1) {
         if (leader()) cnt[idx] += v;
     }
+    __device__ __forceinline__ unsigned long long now() const { return prof ? clock64() : 0ull; }
+    __device__ __forceinline__ void pf_add(int idx, unsigned long long v) {
+        if (prof && leader()) pf[idx] += v;
+    }
 
     // ----------------------------------------------------------- recorder --
     // Recorder::op_begin/lock_acquired/lock_released/op_end
-    // (proj/src/instrumentation.cpp:47-107): one global device clock.
-    __device__ void rec(uint16_t kind, unsigned long long slot) {
-        if (!record || !leader()) return;
+    // (proj/src/instrumentation.cpp:47-107): one global device clock.  Any
+    // lane may record (children are claimed by two lanes).
+    __device__ void rec_lane(uint16_t kind, unsigned long long slot) {
+        if (!record) return;
         const unsigned long long ts = atomicAdd(&hdr->clock, 1ull);
-        const uint32_t idx = rv.event_counts[cur_op];
+        const uint32_t idx = atomicAdd(&rv.event_counts[cur_op], 1u);
         if (idx >= rv.ev_per_op) {
             atomicOr(&hdr->error_flags, (unsigned long long)kErrEventOverflow);
             return;
@@ -100,32 +135,30 @@ struct HeapCta {
         e.kind = kind;
         e.pad = 0;
         e.node = slot;
-        rv.event_counts[cur_op] = idx + 1;
+    }
+    __device__ __forceinline__ void rec(uint16_t kind, unsigned long long slot) {
+        if (record && leader()) rec_lane(kind, slot);
     }
     __device__ void rec_abort() {
-        if (record && leader()) rv.event_counts[cur_op] = 0;
+        if (record && leader()) atomicExch(&rv.event_counts[cur_op], 0u);
     }
 
     // -------------------------------------------------------------- locks --
-    // lock_avail (heap.cpp:98-109): AVAIL -> INUSE.  Leader only.
-    __device__ void lead_lock_avail(unsigned long long slot) {
+    // lock_avail (heap.cpp:98-109): AVAIL -> INUSE.  Calling lane only.
+    __device__ void lane_lock_avail(unsigned long long slot) {
         uint32_t* p = st(slot);
         Backoff b;
         for (;;) {
             if (state_load(p) == kAvail && state_cas(p, kAvail, kInUse)) break;
             b.pause();
         }
-        rec(kEvAcq, slot);
+        rec_lane(kEvAcq, slot);
     }
-    // unlock (heap.cpp:111-114).  Leader only; the caller has passed a
-    // barrier after the CTA's last write to data guarded by this lock.
-    __device__ void lead_unlock(unsigned long long slot, uint32_t release_as = kAvail) {
-        rec(kEvRel, slot);
-        __threadfence();
-        state_store_release(st(slot), release_as);
-    }
-    __device__ void lead_release_only(unsigned long long slot, uint32_t release_as) {
-        __threadfence();
+    // unlock (heap.cpp:111-114).  Calling lane only; the CTA has passed a
+    // barrier after its last write to data guarded by this lock, and the
+    // release store orders those writes before the state change.
+    __device__ __forceinline__ void lane_unlock(unsigned long long slot, uint32_t release_as = kAvail) {
+        rec_lane(kEvRel, slot);
         state_store_release(st(slot), release_as);
     }
 
@@ -142,6 +175,7 @@ struct HeapCta {
 
     // =============================================================== run ==
     __device__ void run() {
+        const unsigned long long t_start = now();
         for (;;) {
             if (leader()) sh->op = atomicAdd(rv.ticket, 1ull);
             __syncthreads();
@@ -156,6 +190,7 @@ struct HeapCta {
                 do_delete(opi, o);
             __syncthreads();
         }
+        pf_add(pfCtaCycles, now() - t_start);
         if (leader()) {
 #pragma unroll
             for (int i = 0; i < kNumCounters; ++i) {
@@ -164,6 +199,11 @@ struct HeapCta {
                 } else if (cnt[i]) {
                     atomicAdd(&hv.counters[i], cnt[i]);
                 }
+            }
+            if (prof) {
+#pragma unroll
+                for (int i = 0; i < kNumProf; ++i)
+                    if (pf[i]) atomicAdd(&hv.prof[i], pf[i]);
             }
         }
     }
@@ -175,6 +215,7 @@ struct HeapCta {
             status(opi, BH_E_CAPACITY, 0, ~0ull);
             return;
         }
+        const unsigned long long t0 = now();
         Key* sorted = buf(0);
         const Key* src = static_cast<const Key*>(rv.key_pool) + o.offset;
         int bad = 0;
@@ -192,39 +233,43 @@ struct HeapCta {
         }
         cta_bitonic_sort<Key, K, T>(sorted);
         rec(kEvInv, 0);
+        const unsigned long long t1 = now();
 
         // ---- root phase (heap.cpp:126-167) ----
         if (leader()) {
-            lead_lock_avail(1);
+            lane_lock_avail(1);
             sh->nodes = ld_cg_u64(&hdr->node_count);
             sh->plen = ld_cg_u64(&hdr->partial_len);
+            sh->seq = ld_cg_u64(&hdr->root_seq);
         }
+        const unsigned long long t2 = now();
         __syncthreads();
         const unsigned long long nodes = sh->nodes;
         const uint32_t plen = (uint32_t)sh->plen;
+        const unsigned long long seq = sh->seq;
         const bool full = n + plen >= (uint32_t)K;
         if (full && nodes == hv.max_nodes) {  // heap.cpp:129-135
-            if (leader()) {
-                rec(kEvRel, 1);
-                lead_release_only(1, kAvail);
-            }
+            if (leader()) lane_unlock(1);
             rec_abort();
             status(opi, BH_E_CAPACITY, 0, ~0ull);
             return;
         }
-        unsigned long long seq = 0;
-        if (leader()) {
-            seq = ld_cg_u64(&hdr->root_seq);
-            st_cg_u64(&hdr->root_seq, seq + 1);
-        }
+        if (leader()) st_cg_u64(&hdr->root_seq, seq + 1);
         count(cInserts);
-        Key* part = buf(1);
-        Key* comb = buf(2);  // 2K wide: buf(2), buf(3)
-        if (plen) cta_load<Key, T>(part, partial, plen);
-        __syncthreads();
-        cta_merge<Key, T>(sorted, n, part, plen, comb, 2 * K, comb);
-        __syncthreads();
+        pf_add(pfInsOps, 1);
+        pf_add(pfInsSort, t1 - t0);
+        pf_add(pfInsRootWait, t2 - t1);
+
         const uint32_t total = n + plen;
+        Key* comb = sorted;  // the combined run; 2K wide when merged (buf 2..3)
+        if (plen) {
+            Key* part = buf(1);
+            comb = buf(2);
+            cta_load<Key, T>(part, partial, plen);
+            __syncthreads();
+            cta_merge<Key, T>(sorted, n, part, plen, comb, 2 * K, comb);
+            __syncthreads();
+        }
 
         if (!full) {
             if (nodes >= 1) {
@@ -246,8 +291,9 @@ struct HeapCta {
             __syncthreads();
             if (leader()) {
                 st_cg_u64(&hdr->partial_len, total);
-                lead_unlock(1);
+                lane_unlock(1);
             }
+            pf_add(pfInsRootHold, now() - t2);
             status(opi, BH_OK, 0, seq);
             rec(kEvRes, 0);
             return;
@@ -257,35 +303,32 @@ struct HeapCta {
         note_partial(total - K);
         const unsigned long long rank = nodes + 1;
         if (leader()) {
-            st_cg_u64(&hdr->partial_len, total - K);
-            st_cg_u64(&hdr->insert_count, ld_cg_u64(&hdr->insert_count) + 1);
+            if (plen || total != (uint32_t)K) st_cg_u64(&hdr->partial_len, total - K);
             st_cg_u64(&hdr->node_count, rank);
         }
         if (rank == 1) {
             cta_store<Key, T>(node(1), comb, K);
             count(cVisits);
             __syncthreads();
-            if (leader()) lead_unlock(1);
+            if (leader()) lane_unlock(1);
+            pf_add(pfInsRootHold, now() - t2);
             status(opi, BH_OK, 0, seq);
             rec(kEvRes, 0);
             return;
         }
         const unsigned long long target = slot_for_rank(rank);
-        // The carried batch lives in comb[0,K) = buf(2); free: 0, 1, 4, 5.
         if (hv.variant == BH_TD)
-            insert_td(target);
+            insert_td(target, comb, t2);
         else
-            insert_bu(target);
+            insert_bu(target, comb, t2);
         status(opi, BH_OK, 0, seq);
         rec(kEvRes, 0);
     }
 
     // merge_step_down (heap.cpp:190-205): node `slot` keeps the k smallest of
-    // node U batch; batch keeps the rest.  `bat` may be rotated with the free
-    // buffers nd/tmp.  Ends with a barrier.
+    // node U batch; the batch keeps the rest.  `nd` must already hold the
+    // node's keys (barrier passed).  Rotates bat/nd/tmp.  Ends with a barrier.
     __device__ void merge_step_down(Key*& bat, Key*& nd, Key*& tmp, unsigned long long slot) {
-        cta_load<Key, T>(nd, node(slot), K);
-        __syncthreads();
         if (slot != 1 && nd[0] == kMaxKey && leader())
             atomicOr(&hdr->error_flags, (unsigned long long)kErrInteriorEmpty);
         if (elide && !needs_merge_full<Key, K>(nd, bat)) {
@@ -307,10 +350,10 @@ struct HeapCta {
     }
 
     // insert_td (heap.cpp:218-293).  Root held on entry.
-    __device__ void insert_td(unsigned long long target) {
-        Key* bat = buf(2);
+    __device__ void insert_td(unsigned long long target, Key* bat, unsigned long long t_root) {
         Key* nd = buf(4);
         Key* tmp = buf(5);
+        if (bat == buf(4)) nd = buf(1);
         if (leader()) {  // claim the target under the root lock
             uint32_t* p = st(target);
             Backoff b;
@@ -319,6 +362,8 @@ struct HeapCta {
                 b.pause();
             }
         }
+        cta_load<Key, T>(nd, node(1), K);  // root keys, in the claim's round trip
+        __syncthreads();
         merge_step_down(bat, nd, tmp, 1);
         count(cVisits);
         unsigned long long cur = 1;
@@ -372,33 +417,38 @@ struct HeapCta {
                 count(cCoop);
                 __syncthreads();
                 if (leader()) {
-                    lead_release_only(target, kAvail);
-                    lead_unlock(cur);
+                    state_store_release(st(target), kAvail);
+                    lane_unlock(cur);
                 }
+                if (cur == 1) pf_add(pfInsRootHold, now() - t_root);
                 return;
             }
             if (act == kWrite) {
                 if (leader()) {
                     rec(kEvAcq, target);
-                    lead_unlock(cur);
+                    lane_unlock(cur);
                 }
+                if (cur == 1) pf_add(pfInsRootHold, now() - t_root);
                 cta_store<Key, T>(node(target), bat, K);
                 count(cVisits);
                 __syncthreads();
-                if (leader()) lead_unlock(target);
+                if (leader()) lane_unlock(target);
                 return;
             }
             if (act == kSkip) continue;
             if (leader()) rec(kEvAcq, next);
+            cta_load<Key, T>(nd, node(next), K);
+            __syncthreads();
             merge_step_down(bat, nd, tmp, next);
             count(cVisits);
-            if (leader()) lead_unlock(cur);
+            if (leader()) lane_unlock(cur);
+            if (cur == 1) pf_add(pfInsRootHold, now() - t_root);
             cur = next;
         }
     }
 
-    // abandon_park (heap.cpp:393-407).  Leader only.
-    __device__ void lead_abandon_park(unsigned long long slot) {
+    // abandon_park (heap.cpp:393-407).  Calling lane only.
+    __device__ void lane_abandon_park(unsigned long long slot) {
         Backoff b;
         for (;;) {
             const uint32_t s = state_load(st(slot));
@@ -413,9 +463,8 @@ struct HeapCta {
     }
 
     // insert_bu (heap.cpp:295-373).  Root held on entry.
-    __device__ void insert_bu(unsigned long long target) {
-        Key* bat = buf(2);
-        Key* par = buf(4);
+    __device__ void insert_bu(unsigned long long target, Key* bat, unsigned long long t_root) {
+        Key* par = bat == buf(4) ? buf(1) : buf(4);
         Key* cu = buf(5);
         if (leader()) {
             uint32_t* p = st(target);
@@ -427,19 +476,21 @@ struct HeapCta {
                 b.pause();
             }
             rec(kEvAcq, target);
+            // The target is ours (INUSE): let the root go before writing it.
+            lane_unlock(1);
         }
+        pf_add(pfInsRootHold, now() - t_root);
+        const unsigned long long t3 = now();
         cta_store<Key, T>(node(target), bat, K);
         count(cVisits);
         __syncthreads();
-        if (leader()) lead_unlock(1);
 
         unsigned long long cur = target;  // held
         while (cur != 1) {
             const unsigned long long parent = cur >> 1;
             if (leader()) {
                 // park: others may take the slot meanwhile
-                rec(kEvRel, cur);
-                lead_release_only(cur, kInsHold);
+                lane_unlock(cur, kInsHold);
                 uint32_t* pp = st(parent);
                 Backoff b;
                 for (;;) {
@@ -456,9 +507,10 @@ struct HeapCta {
             if (par[0] == kMaxKey) {
                 // parent was deleted: the subtree with our parked slot is gone
                 if (leader()) {
-                    lead_unlock(parent);
-                    lead_abandon_park(cur);
+                    lane_unlock(parent);
+                    lane_abandon_park(cur);
                 }
+                pf_add(pfInsRest, now() - t3);
                 return;
             }
             if (leader()) {
@@ -492,12 +544,10 @@ struct HeapCta {
                 if (cu[0] >= par[K - 1]) {
                     count(cEarlyStops);
                     if (leader()) {
-                        rec(kEvRel, cur);
-                        rec(kEvRel, parent);
-                        __threadfence();
-                        state_store_release(st(cur), kAvail);
-                        state_store_release(st(parent), kAvail);
+                        lane_unlock(cur);
+                        lane_unlock(parent);
                     }
+                    pf_add(pfInsRest, now() - t3);
                     return;
                 }
                 // merge_step_up (heap.cpp:375-391): parent keeps the k smallest
@@ -511,153 +561,18 @@ struct HeapCta {
                 }
                 count(cVisits);
                 __syncthreads();
-                if (leader()) lead_unlock(cur);
+                if (leader()) lane_unlock(cur);
             }
             cur = parent;
         }
-        if (leader()) lead_unlock(1);
+        if (leader()) lane_unlock(1);
+        pf_add(pfInsRest, now() - t3);
     }
 
     // ============================================================ delete ==
-    __device__ void do_delete(unsigned long long opi, const bh_op& o) {
-        rec(kEvInv, 0);
-        if (leader()) {
-            lead_lock_avail(1);
-            sh->nodes = ld_cg_u64(&hdr->node_count);
-            sh->plen = ld_cg_u64(&hdr->partial_len);
-            const unsigned long long seq = ld_cg_u64(&hdr->root_seq);
-            st_cg_u64(&hdr->root_seq, seq + 1);
-            sh->seq = seq;
-        }
-        __syncthreads();
-        const unsigned long long nodes = sh->nodes;
-        const uint32_t plen = (uint32_t)sh->plen;
-        const unsigned long long seq = sh->seq;
-        Key* out = static_cast<Key*>(rv.out_pool) + o.offset;
-
-        if (nodes == 0) {
-            if (plen == 0) {  // empty heap (heap.cpp:424-429)
-                if (leader()) lead_unlock(1);
-                status(opi, BH_E_EMPTY, 0, seq);
-                rec(kEvRes, 0);
-                return;
-            }
-            // fewer than k keys: they all live in the partial buffer
-            cta_copy_gg<Key, T>(out, partial, plen);
-            count(cDeletes);
-            __syncthreads();
-            if (leader()) {
-                st_cg_u64(&hdr->partial_len, 0);
-                st_cg_u64(&hdr->delete_count, ld_cg_u64(&hdr->delete_count) + 1);
-                lead_unlock(1);
-            }
-            status(opi, BH_OK, plen, seq);
-            rec(kEvRes, 0);
-            return;
-        }
-
-        int ci = 0;  // buffer index holding the carried (cur) batch
-        Key* cur_s = buf(ci);
-        cta_load<Key, T>(cur_s, node(1), K);
-        __syncthreads();
-        cta_store<Key, T>(out, cur_s, K);
-        if (leader() && cur_s[K - 1] == kMaxKey)
-            atomicOr(&hdr->error_flags, (unsigned long long)kErrSentinelEscaped);
-        count(cDeletes);
-        if (leader()) {
-            st_cg_u64(&hdr->delete_count, ld_cg_u64(&hdr->delete_count) + 1);
-            st_cg_u64(&hdr->node_count, nodes - 1);
-        }
-        if (nodes == 1) {
-            cta_fill<Key, T>(node(1), kMaxKey, K);
-            __syncthreads();
-            if (leader()) lead_unlock(1);
-            status(opi, BH_OK, K, seq);
-            rec(kEvRes, 0);
-            return;
-        }
-
-        // ---- refill_root_from(last) (heap.cpp:467-531) ----
-        const unsigned long long last = slot_for_rank(nodes);
-        enum { kTake = 1, kCoop = 2 };
-        if (leader()) {
-            uint32_t* p = st(last);
-            uint32_t act = 0, rel = kAvail;
-            Backoff b;
-            for (;;) {
-                const uint32_t s = state_load(p);
-                if (s == kAvail) {
-                    if (state_cas(p, kAvail, kInUse)) {
-                        act = kTake;
-                        break;
-                    }
-                } else if (hv.variant == BH_TD && s == kTarget) {
-                    if (state_cas(p, kTarget, kMarked)) {
-                        act = kCoop;
-                        break;
-                    }
-                } else if (hv.variant == BH_BU && s == kInsHold) {
-                    if (state_cas(p, kInsHold, kInUse)) {  // take the in-flight batch
-                        act = kTake;
-                        rel = kDelMod;
-                        break;
-                    }
-                } else if (hv.variant == BH_BU && s == kDelMod) {
-                    if (state_cas(p, kDelMod, kInUse)) {
-                        act = kTake;
-                        break;
-                    }
-                } else {
-                    b.pause();
-                }
-            }
-            if (act == kCoop) {
-                // the inserter ships its batch into the root, then AVAIL
-                Backoff w;
-                while (state_load(p) != kAvail) w.pause();
-            } else {
-                rec(kEvAcq, last);
-            }
-            sh->act = act;
-            sh->lrel = rel;
-        }
-        __syncthreads();
-        if (sh->act == kTake) {
-            cta_load<Key, T>(cur_s, node(last), K);
-            __syncthreads();
-            cta_fill<Key, T>(node(last), kMaxKey, K);
-            __syncthreads();
-            if (leader()) lead_unlock(last, sh->lrel);
-        } else {
-            cta_load<Key, T>(cur_s, node(1), K);
-            __syncthreads();
-        }
-
-        // ---- remerge_root_with_partial (heap.cpp:533-545) ----
-        if (plen) {
-            Key* sp = buf(1);
-            Key* tmp = buf(2);
-            cta_load<Key, T>(sp, partial, plen);
-            __syncthreads();
-            if (elide && sp[0] >= cur_s[K - 1]) {
-                count(cElided);
-            } else {
-                cta_merge<Key, T>(cur_s, K, sp, plen, tmp, K, partial);
-                count(cMerges);
-                note_partial(plen);
-                ci = 2;
-                cur_s = tmp;
-            }
-            __syncthreads();
-        }
-        heapify_down(ci);
-        status(opi, BH_OK, K, seq);
-        rec(kEvRes, 0);
-    }
-
-    // acquire_child (heap.cpp:547-585).  Leader only.  Returns locked?;
-    // rel = state to release with.
-    __device__ uint32_t lead_acquire_child(unsigned long long slot, uint32_t& rel) {
+    // acquire_child (heap.cpp:547-585).  Calling lane only.  Returns
+    // locked?; rel = state to release with.
+    __device__ uint32_t lane_acquire_child(unsigned long long slot, uint32_t& rel) {
         rel = kAvail;
         if (slot > hv.slot_count) return 0;
         uint32_t* p = st(slot);
@@ -679,34 +594,224 @@ struct HeapCta {
                 b.pause();
             }
         }
-        rec(kEvAcq, slot);
+        rec_lane(kEvAcq, slot);
         return 1;
     }
 
-    // heapify_down (heap.cpp:591-667) with the carried batch in buf(ci).
-    // Root held on entry; all held locks are released on exit.
-    __device__ void heapify_down(int ci) {
-        unsigned long long cur = 1;
-        uint32_t cur_rel = kAvail;
+    // Claims both children of `cur` with lanes 0 and 1 of warp 0.
+    __device__ void acquire_children(unsigned long long cur) {
+        if (threadIdx.x < 2) {
+            const unsigned long long t = now();
+            uint32_t rel;
+            const uint32_t got = lane_acquire_child(2 * cur + threadIdx.x, rel);
+            if (threadIdx.x == 0) {
+                sh->lk = got;
+                sh->lrel = rel;
+                if (prof) pf[pfChildWait] += clock64() - t;
+            } else {
+                sh->rk = got;
+                sh->rrel = rel;
+            }
+        }
+    }
+
+    // refill_root_from(last) claim (heap.cpp:467-531).  Calling lane only.
+    enum { kTake = 1, kCoop = 2 };
+    __device__ void lane_claim_last(unsigned long long last) {
+        uint32_t* p = st(last);
+        uint32_t act = 0, rel = kAvail;
+        Backoff b;
         for (;;) {
-            Key* cur_s = buf(ci);
-            Key* L = buf((ci + 1) % kBufs);
-            Key* R = buf((ci + 2) % kBufs);
-            Key* H = buf((ci + 3) % kBufs);
-            Key* nx = buf((ci + 4) % kBufs);
-            const unsigned long long l = 2 * cur, r = 2 * cur + 1;
+            const uint32_t s = state_load(p);
+            if (s == kAvail) {
+                if (state_cas(p, kAvail, kInUse)) {
+                    act = kTake;
+                    break;
+                }
+            } else if (hv.variant == BH_TD && s == kTarget) {
+                if (state_cas(p, kTarget, kMarked)) {
+                    act = kCoop;
+                    break;
+                }
+            } else if (hv.variant == BH_BU && s == kInsHold) {
+                if (state_cas(p, kInsHold, kInUse)) {  // take the in-flight batch
+                    act = kTake;
+                    rel = kDelMod;
+                    break;
+                }
+            } else if (hv.variant == BH_BU && s == kDelMod) {
+                if (state_cas(p, kDelMod, kInUse)) {
+                    act = kTake;
+                    break;
+                }
+            } else {
+                b.pause();
+            }
+        }
+        if (act == kCoop) {
+            // the inserter ships its batch into the root, then AVAIL
+            Backoff w;
+            while (state_load(p) != kAvail) w.pause();
+        } else {
+            rec_lane(kEvAcq, last);
+        }
+        sh->act = act;
+        sh->lastrel = rel;
+    }
+
+    __device__ void do_delete(unsigned long long opi, const bh_op& o) {
+        const unsigned long long t0 = now();
+        rec(kEvInv, 0);
+        if (leader()) lane_lock_avail(1);
+        const unsigned long long t1 = now();
+        __syncthreads();
+        // the root batch, read in the same round trip as the header
+        Key* cur_s = buf(0);
+        if (leader()) {
+            sh->nodes = ld_cg_u64(&hdr->node_count);
+            sh->plen = ld_cg_u64(&hdr->partial_len);
+            sh->seq = ld_cg_u64(&hdr->delete_count);
+        }
+        cta_load<Key, T>(cur_s, node(1), K);
+        __syncthreads();
+        const unsigned long long nodes = sh->nodes;
+        const uint32_t plen = (uint32_t)sh->plen;
+        const unsigned long long seq = sh->seq;
+        Key* out = static_cast<Key*>(rv.out_pool) + o.offset;
+        pf_add(pfDelOps, 1);
+        pf_add(pfDelRootWait, t1 - t0);
+
+        if (nodes == 0) {
+            if (plen == 0) {  // empty heap (heap.cpp:424-429)
+                if (leader()) lane_unlock(1);
+                pf_add(pfDelRootHold, now() - t1);
+                status(opi, BH_E_EMPTY, 0, ~0ull);
+                rec(kEvRes, 0);
+                return;
+            }
+            // fewer than k keys: they all live in the partial buffer
+            cta_copy_gg<Key, T>(out, partial, plen);
+            count(cDeletes);
+            __syncthreads();
             if (leader()) {
-                uint32_t lrel, rrel;
-                sh->lk = lead_acquire_child(l, lrel);
-                sh->rk = lead_acquire_child(r, rrel);
-                sh->lrel = lrel;
-                sh->rrel = rrel;
+                st_cg_u64(&hdr->partial_len, 0);
+                st_cg_u64(&hdr->delete_count, seq + 1);
+                lane_unlock(1);
+            }
+            pf_add(pfDelRootHold, now() - t1);
+            status(opi, BH_OK, plen, seq);
+            rec(kEvRes, 0);
+            return;
+        }
+
+        cta_store<Key, T>(out, cur_s, K);  // the result: the root's k keys
+        if (leader()) {
+            if (cur_s[K - 1] == kMaxKey)
+                atomicOr(&hdr->error_flags, (unsigned long long)kErrSentinelEscaped);
+            st_cg_u64(&hdr->delete_count, seq + 1);
+            st_cg_u64(&hdr->node_count, nodes - 1);
+        }
+        count(cDeletes);
+        if (nodes == 1) {
+            cta_fill<Key, T>(node(1), kMaxKey, K);
+            __syncthreads();
+            if (leader()) lane_unlock(1);
+            pf_add(pfDelRootHold, now() - t1);
+            status(opi, BH_OK, K, seq);
+            rec(kEvRes, 0);
+            return;
+        }
+
+        const unsigned long long last = slot_for_rank(nodes);
+        Key* L = buf(1);
+        Key* R = buf(2);
+        Key* sp = buf(3);
+        bool pre = false;
+        if (last >= 4) {
+            // Claim children 2 and 3 (two lanes), then the last node: the
+            // same ancestor-first order as every other walk.
+            acquire_children(1);
+            __syncthreads();
+            if (leader()) lane_claim_last(last);
+            __syncthreads();
+            pre = true;
+            if (sh->lk) cta_load<Key, T>(L, node(2), K);
+            if (sh->rk) cta_load<Key, T>(R, node(3), K);
+        } else {
+            __syncthreads();
+            if (leader()) lane_claim_last(last);
+            __syncthreads();
+        }
+        const uint32_t act = sh->act;
+        cta_load<Key, T>(cur_s, node(act == kTake ? last : 1), K);
+        if (plen) cta_load<Key, T>(sp, partial, plen);
+        __syncthreads();
+        if (act == kTake) {
+            cta_fill<Key, T>(node(last), kMaxKey, K);
+            __syncthreads();
+            if (leader()) lane_unlock(last, sh->lastrel);
+        }
+
+        // ---- remerge_root_with_partial (heap.cpp:533-545) ----
+        int ci = 0;
+        if (plen) {
+            if (elide && sp[0] >= cur_s[K - 1]) {
+                count(cElided);
+            } else {
+                Key* tmp = buf(5);
+                cta_merge<Key, T>(cur_s, K, sp, plen, tmp, K, partial);
+                count(cMerges);
+                note_partial(plen);
+                ci = 5;
             }
             __syncthreads();
+        }
+        heapify_down(ci, pre, t1);
+        status(opi, BH_OK, K, seq);
+        rec(kEvRes, 0);
+    }
+
+    // heapify_down (heap.cpp:591-667) with the carried batch in buf(ci).
+    // Root held on entry; with `pre`, the root's children were claimed and
+    // loaded into buf(1)/buf(2) by the caller.  Releases every lock it holds.
+    __device__ void heapify_down(int ci, bool pre, unsigned long long t_root) {
+        unsigned long long cur = 1;
+        uint32_t cur_rel = kAvail;
+        const unsigned long long t_start = now();
+        for (;;) {
+            // buffer plan: L, R, H, NX distinct from the carried batch
+            int li, ri, hx, nxi;
+            if (pre) {
+                li = 1;
+                ri = 2;
+                int f[3], nf = 0;
+                for (int i = 0; i < kBufs && nf < 3; ++i)
+                    if (i != ci && i != 1 && i != 2) f[nf++] = i;
+                hx = f[0];
+                nxi = f[1];
+            } else {
+                int f[4], nf = 0;
+                for (int i = 0; i < kBufs && nf < 4; ++i)
+                    if (i != ci) f[nf++] = i;
+                li = f[0];
+                ri = f[1];
+                hx = f[2];
+                nxi = f[3];
+            }
+            Key* cur_s = buf(ci);
+            Key* L = buf(li);
+            Key* R = buf(ri);
+            const unsigned long long l = 2 * cur, r = 2 * cur + 1;
+            if (!pre) {
+                acquire_children(cur);
+                __syncthreads();
+                if (sh->lk) cta_load<Key, T>(L, node(l), K);
+                if (sh->rk) cta_load<Key, T>(R, node(r), K);
+                __syncthreads();
+            }
+            pre = false;
+            pf_add(pfLevels, 1);
             const uint32_t lk = sh->lk, rk = sh->rk;
-            if (lk) cta_load<Key, T>(L, node(l), K);
-            if (rk) cta_load<Key, T>(R, node(r), K);
-            __syncthreads();
             const bool lempty = !lk || L[0] == kMaxKey;
             const bool rempty = !rk || R[0] == kMaxKey;
             const Key cmax = cur_s[K - 1];
@@ -723,42 +828,36 @@ struct HeapCta {
                 cta_store<Key, T>(node(cur), cur_s, K);
                 __syncthreads();
                 if (leader()) {
-                    if (lk) rec(kEvRel, l);
-                    if (rk) rec(kEvRel, r);
-                    rec(kEvRel, cur);
-                    __threadfence();
-                    if (lk) state_store_release(st(l), sh->lrel);
-                    if (rk) state_store_release(st(r), sh->rrel);
-                    state_store_release(st(cur), cur_rel);
+                    if (lk) lane_unlock(l, sh->lrel);
+                    if (rk) lane_unlock(r, sh->rrel);
+                    lane_unlock(cur, cur_rel);
                 }
+                if (cur == 1) pf_add(pfDelRootHold, now() - t_root);
+                pf_add(pfDelRest, now() - t_start);
                 return;
             }
             // Merge the children: lo lands in the child whose max was larger
             // (right on ties), hi in the other, which we descend into.
             bool hi_left;
             Key* hdata;
-            int hidx;
             if (lempty) {
                 hi_left = false;
                 hdata = R;
-                hidx = (ci + 2) % kBufs;
             } else if (rempty) {
                 hi_left = true;
                 hdata = L;
-                hidx = (ci + 1) % kBufs;
             } else if (elide && !needs_merge_full<Key, K>(L, R)) {
                 count(cElided);
                 // fix of heap.cpp:628-636: the batch with the smaller keys is hi
                 hi_left = L[K - 1] <= R[0];
                 hdata = hi_left ? L : R;
-                hidx = hi_left ? (ci + 1) % kBufs : (ci + 2) % kBufs;
             } else {
                 hi_left = !(L[K - 1] > R[K - 1]);
+                Key* H = buf(hx);
                 cta_merge_full<Key, K, T>(L, R, H, node(hi_left ? r : l));
                 count(cMerges);
                 __syncthreads();
                 hdata = H;
-                hidx = (ci + 3) % kBufs;
             }
             const unsigned long long hi = hi_left ? l : r;
             const unsigned long long lo = hi_left ? r : l;
@@ -770,26 +869,23 @@ struct HeapCta {
                 cta_store<Key, T>(node(cur), hdata, K);
                 next_ci = ci;  // old cur batch moves down into hi
             } else {
-                cta_merge_full<Key, K, T>(cur_s, hdata, node(cur), nx);
+                cta_merge_full<Key, K, T>(cur_s, hdata, node(cur), buf(nxi));
                 count(cMerges);
-                next_ci = (ci + 4) % kBufs;
+                next_ci = nxi;
             }
-            (void)hidx;
             count(cVisits);
             __syncthreads();
             const uint32_t hi_rel = hi_left ? sh->lrel : sh->rrel;
             if (leader()) {
                 const uint32_t lo_rel = hi_left ? sh->rrel : sh->lrel;
-                if (lo_locked) rec(kEvRel, lo);
-                rec(kEvRel, cur);
-                __threadfence();
-                if (lo_locked) state_store_release(st(lo), lo_rel);
-                state_store_release(st(cur), cur_rel);
+                if (lo_locked) lane_unlock(lo, lo_rel);
+                lane_unlock(cur, cur_rel);
             }
+            if (cur == 1) pf_add(pfDelRootHold, now() - t_root);
             cur = hi;
             cur_rel = hi_rel;
             ci = next_ci;
-            __syncthreads();  // sh->lrel/rrel reused next level
+            __syncthreads();  // sh->lk/rk/lrel/rrel are rewritten next level
         }
     }
 };

@@ -70,6 +70,7 @@ struct HeapView {
     Header* hdr;
     void* partial;           // k keys
     unsigned long long* counters;
+    unsigned long long* prof;  // non-null on BH_FLAG_PROFILE handles
     unsigned long long slot_count;
     uint32_t k;
     uint32_t max_nodes;

@@ -8,6 +8,9 @@
 
 namespace bh {
 
+// Records a CUDA error for the C ABI's message; BH_OK on cudaSuccess.
+int note_cuda(cudaError_t e);
+
 // Standalone sort_batch over rows of stride K (proj/src/batch.cpp:7-19).
 template <typename Key, int K, int T>
 __global__ void __launch_bounds__(T) sort_rows_kernel(Key* keys, const uint32_t* lens,
@@ -96,26 +99,22 @@ template <typename Key, int K>
 int launch_ops_k(const HeapView& hv, const RunView& rv, uint32_t ctas, cudaStream_t stream) {
     using Cfg = KernelCfg<Key, K>;
     auto kern = heap_ops_kernel<Key, K, Cfg::kThreads>;
-    if (Cfg::kSmem > 48 * 1024) {
-        static bool attr_set = false;
-        if (!attr_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
-                cudaSuccess)
-                return BH_E_CUDA;
-            attr_set = true;
-        }
+    static bool attr_set = false;  // dynamic + static smem may pass 48 KB
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        if (e != cudaSuccess) return note_cuda(e);
+        attr_set = true;
     }
     kern<<<ctas, Cfg::kThreads, Cfg::kSmem, stream>>>(hv, rv);
-    return cudaGetLastError() == cudaSuccess ? BH_OK : BH_E_CUDA;
+    return note_cuda(cudaGetLastError());
 }
 
 template <typename Key, int K>
 int kernel_info_k(KernelInfo* info) {
     using Cfg = KernelCfg<Key, K>;
     auto kern = heap_ops_kernel<Key, K, Cfg::kThreads>;
-    if (Cfg::kSmem > 48 * 1024 &&
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
-        return BH_E_CUDA;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (e != cudaSuccess) return note_cuda(e);
     int blocks = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, Cfg::kThreads, Cfg::kSmem) !=
         cudaSuccess)
@@ -134,7 +133,7 @@ int launch_sort_k(void* keys, const uint32_t* lens, uint64_t rows, cudaStream_t 
     if (grid == 0) return BH_OK;
     sort_rows_kernel<Key, K, Cfg::kThreads>
         <<<grid, Cfg::kThreads, smem, stream>>>(static_cast<Key*>(keys), lens, rows);
-    return cudaGetLastError() == cudaSuccess ? BH_OK : BH_E_CUDA;
+    return note_cuda(cudaGetLastError());
 }
 
 template <typename Key, int K>
@@ -142,14 +141,15 @@ int launch_merge_k(const void* a, const void* b, void* hi, void* lo, uint64_t ro
     using Cfg = KernelCfg<Key, K>;
     const uint32_t smem = 2 * K * sizeof(Key);
     auto kern = merge_rows_kernel<Key, K, Cfg::kThreads>;
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-        return BH_E_CUDA;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return note_cuda(e);
+    }
     const unsigned grid = (unsigned)(rows < 148ull * 16 ? rows : 148ull * 16);
     if (grid == 0) return BH_OK;
     kern<<<grid, Cfg::kThreads, smem, stream>>>(static_cast<const Key*>(a), static_cast<const Key*>(b),
                                                 static_cast<Key*>(hi), static_cast<Key*>(lo), rows);
-    return cudaGetLastError() == cudaSuccess ? BH_OK : BH_E_CUDA;
+    return note_cuda(cudaGetLastError());
 }
 
 #define BH_FOR_EACH_K(X) \
@@ -207,7 +207,7 @@ int dispatch_merge(uint32_t k, const void* a, const void* b, void* hi, void* lo,
 template <typename Key>
 int launch_check(const HeapView& hv, unsigned long long* result, cudaStream_t s) {
     check_kernel<Key><<<148 * 4, 256, 0, s>>>(hv, result);
-    return cudaGetLastError() == cudaSuccess ? BH_OK : BH_E_CUDA;
+    return note_cuda(cudaGetLastError());
 }
 
 template <typename Key>
@@ -215,7 +215,7 @@ int launch_gather(const HeapView& hv, unsigned long long nodes, void* out, cudaS
     if (nodes == 0) return BH_OK;
     const unsigned grid = (unsigned)(nodes < 148ull * 8 ? nodes : 148ull * 8);
     gather_kernel<Key><<<grid, 256, 0, s>>>(hv, nodes, static_cast<Key*>(out));
-    return cudaGetLastError() == cudaSuccess ? BH_OK : BH_E_CUDA;
+    return note_cuda(cudaGetLastError());
 }
 
 }  // namespace bh

@@ -114,10 +114,10 @@ class GeneralizedHeap:
 
     def __init__(self, variant: Variant, k: int, max_nodes: int,
                  options: Optional[HeapOptions] = None, record: bool = False,
-                 key_bits: int = 64, device: int = 0):
+                 key_bits: int = 64, device: int = 0, profile: bool = False):
         options = options or HeapOptions()
         flags = (L.BH_FLAG_ELIDE_MERGES if options.elide_merges else 0) | \
-                (L.BH_FLAG_RECORD if record else 0)
+                (L.BH_FLAG_RECORD if record else 0) | (L.BH_FLAG_PROFILE if profile else 0)
         h = C.c_void_p()
         _raise(L.lib().bh_create(C.byref(h), int(variant), int(k), int(max_nodes),
                                  int(key_bits), flags, int(device)))
@@ -200,10 +200,11 @@ class GeneralizedHeap:
 
     def run_ops_ptr(self, ops_ptr: int, n_ops: int, pool_ptr: int, out_ptr: int,
                     status_ptr: int = 0, lens_ptr: int = 0, seq_ptr: int = 0,
-                    ctas: int = 0, stream: int = 0) -> None:
+                    ctas: int = 0, stream: Optional[int] = None) -> None:
         """Bulk submission with DEVICE pointers (e.g. torch ``data_ptr()``),
-        asynchronous on ``stream`` (a cudaStream_t as int)."""
-        cfg = L.bh_run_cfg(ctas, 0, stream or None)
+        asynchronous on ``stream`` (a cudaStream_t as int; 0 is the legacy
+        default stream; None the handle's own stream)."""
+        cfg = L.bh_run_cfg(ctas, 0 if stream is None else L.BH_RUN_EXPLICIT_STREAM, stream or None)
         _raise(L.lib().bh_run_ops_device(self._h, ops_ptr, n_ops, pool_ptr or None, out_ptr or None,
                                          status_ptr or None, lens_ptr or None, seq_ptr or None,
                                          C.byref(cfg)))
@@ -270,6 +271,16 @@ class GeneralizedHeap:
         ev = np.empty(max(n.value, 1), dtype=EVENT_DTYPE)
         _raise(L.lib().bh_history(self._h, ev.ctypes.data_as(C.c_void_p), ev.size, C.byref(n)))
         return ev[:n.value]
+
+    PROFILE_FIELDS = ("ins_ops", "ins_sort", "ins_root_wait", "ins_root_hold", "ins_rest",
+                      "del_ops", "del_root_wait", "del_root_hold", "del_rest", "child_wait",
+                      "levels", "cta_cycles")
+
+    def profile(self, reset: bool = True) -> dict:
+        """SM-cycle profile of a BH_FLAG_PROFILE heap (see bh_profile)."""
+        buf = (C.c_uint64 * 32)()
+        _raise(L.lib().bh_profile(self._h, buf, 32, int(reset)))
+        return dict(zip(self.PROFILE_FIELDS, (int(v) for v in buf)))
 
     def info(self) -> dict:
         k, kb, mn, tpc, mc = (C.c_uint32() for _ in range(5))

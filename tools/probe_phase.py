@@ -17,6 +17,7 @@ ap.add_argument("--k", type=int, nargs="+", default=[1024])
 ap.add_argument("--variant", default="bu")
 ap.add_argument("--ctas", type=int, nargs="+", default=[0])
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--profile", action="store_true")
 a = ap.parse_args()
 n = 1 << a.log2n
 dev = torch.device("cuda")
@@ -25,7 +26,7 @@ pool = torch.from_numpy(keys.view(np.int32)).to(dev)
 for k in a.k:
     for ctas in a.ctas:
         for rep in range(a.reps):
-            heap = GeneralizedHeap(Variant.BU if a.variant == "bu" else Variant.TD, k, n // k + 1024, key_bits=32)
+            heap = GeneralizedHeap(Variant.BU if a.variant == "bu" else Variant.TD, k, n // k + 1024, key_bits=32, profile=a.profile)
             n_ops = n // k
             ops_i = torch.from_numpy(phase_ops(0, n, k).view(np.uint8)).to(dev)
             ops_d = torch.from_numpy(phase_ops(1, n, k).view(np.uint8)).to(dev)
@@ -50,4 +51,14 @@ for k in a.k:
                   f"delete {td:.2f} ms  key-ops/s {2*n/((ti+td)/1e3):.3e} sorted={ok} "
                   f"merges={c.merges} elided={c.elided_merges} early={c.early_stops} visits={c.propagation_node_visits}",
                   flush=True)
+            if a.profile:
+                p = heap.profile()
+                ghz = 1.9
+                def us(c, ops):
+                    return c / max(ops, 1) / (ghz * 1e3)
+                print(f"   ins/op us: sort {us(p['ins_sort'], p['ins_ops']):.2f} rootwait {us(p['ins_root_wait'], p['ins_ops']):.2f} "
+                      f"roothold {us(p['ins_root_hold'], p['ins_ops']):.2f} rest {us(p['ins_rest'], p['ins_ops']):.2f} | "
+                      f"del/op us: rootwait {us(p['del_root_wait'], p['del_ops']):.2f} roothold {us(p['del_root_hold'], p['del_ops']):.2f} "
+                      f"heapify {us(p['del_rest'], p['del_ops']):.2f} childwait {us(p['child_wait'], p['del_ops']):.2f} "
+                      f"levels/del {p['levels']/max(p['del_ops'],1):.2f}", flush=True)
             heap.close()
