@@ -104,6 +104,7 @@ struct bh_heap {
     unsigned long long slot_count = 0;
     void* d_keys = nullptr;
     uint32_t* d_states = nullptr;
+    uint32_t* d_root_flags = nullptr;
     Header* d_hdr = nullptr;
     void* d_partial = nullptr;
     unsigned long long* d_counters = nullptr;
@@ -136,6 +137,7 @@ struct bh_heap {
         HeapView v;
         v.keys = d_keys;
         v.states = d_states;
+        v.root_flags = d_root_flags;
         v.hdr = d_hdr;
         v.partial = d_partial;
         v.counters = d_counters;
@@ -377,6 +379,11 @@ int bh_create(bh_heap** out, int variant, uint32_t k, uint32_t max_nodes, uint32
     cudaMemsetAsync(h->d_hdr, 0, sizeof(Header), h->stream);
     cudaMemsetAsync(h->d_partial, 0xFF, std::max<size_t>((size_t)k * h->key_size, 16), h->stream);
     cudaMemsetAsync(h->d_counters, 0, kNumCounters * 8, h->stream);
+    // root queue lock: slot 0 admits ticket 0, every other slot admits nobody
+    if ((e = cudaMalloc(&h->d_root_flags, (size_t)kRootQueue * kRootFlagStride * 4)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "root flags"));
+    cudaMemsetAsync(h->d_root_flags, 0xFF, (size_t)kRootQueue * kRootFlagStride * 4, h->stream);
+    cudaMemsetAsync(h->d_root_flags, 0, 4, h->stream);
     if (flags & BH_FLAG_PROFILE) {
         if ((e = cudaMalloc(&h->d_prof, 32 * 8)) != cudaSuccess) return cleanup(cuda_fail(e, "prof"));
         cudaMemsetAsync(h->d_prof, 0, 32 * 8, h->stream);
@@ -405,6 +412,7 @@ void bh_destroy(bh_heap* h) {
     }
     cudaFree(h->d_keys);
     cudaFree(h->d_states);
+    cudaFree(h->d_root_flags);
     cudaFree(h->d_hdr);
     cudaFree(h->d_partial);
     cudaFree(h->d_counters);

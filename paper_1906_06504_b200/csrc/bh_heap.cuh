@@ -63,6 +63,15 @@ enum ProfIdx {
     pfChildWait,
     pfLevels,
     pfCtaCycles,
+    pfRsHead,   // delete root step: root lock -> header/root batch in smem
+    pfRsChild,  //   claim children 2 and 3
+    pfRsLast,   //   claim the last node
+    pfRsLoad,   //   load children/refill/partial
+    pfRsFill,   //   sentinel-fill + release of the last node, partial re-merge
+    pfLvAcq,    // heapify level: claim children
+    pfLvLoad,   //   load children
+    pfLvMerge,  //   both merges
+    pfLvRel,    //   write-back barrier + releases
     kNumProf
 };
 
@@ -144,8 +153,33 @@ struct HeapCta {
     }
 
     // -------------------------------------------------------------- locks --
+    // The root only ever takes AVAIL <-> INUSE (every op starts there and no
+    // walk treats it as a child or refill source), so its lock is a FIFO
+    // array queue lock: each waiter spins on its own 128-byte flag instead
+    // of every CTA hammering one L2 word with CAS, and the hand-off costs one
+    // store.  Mutual exclusion and FIFO hand-off order are the reference's
+    // lock_avail(1)/unlock(1) semantics (heap.cpp:98-114).  Leader lane only.
+    unsigned long long root_ticket = 0;
+    __device__ void root_lock() {
+        const unsigned long long t = atomicAdd(&hdr->root_tail, 1ull);
+        uint32_t* f = hv.root_flags + (t % kRootQueue) * kRootFlagStride;
+        Backoff b;
+        while (state_load(f) != (uint32_t)t) b.pause();
+        root_ticket = t;
+        rec_lane(kEvAcq, 1);
+    }
+    __device__ void root_unlock() {
+        rec_lane(kEvRel, 1);
+        const unsigned long long nt = root_ticket + 1;
+        state_store_release(hv.root_flags + (nt % kRootQueue) * kRootFlagStride, (uint32_t)nt);
+    }
+
     // lock_avail (heap.cpp:98-109): AVAIL -> INUSE.  Calling lane only.
     __device__ void lane_lock_avail(unsigned long long slot) {
+        if (slot == 1) {
+            root_lock();
+            return;
+        }
         uint32_t* p = st(slot);
         Backoff b;
         for (;;) {
@@ -158,6 +192,10 @@ struct HeapCta {
     // barrier after its last write to data guarded by this lock, and the
     // release store orders those writes before the state change.
     __device__ __forceinline__ void lane_unlock(unsigned long long slot, uint32_t release_as = kAvail) {
+        if (slot == 1) {
+            root_unlock();
+            return;
+        }
         rec_lane(kEvRel, slot);
         state_store_release(st(slot), release_as);
     }
@@ -477,10 +515,11 @@ struct HeapCta {
             }
             rec(kEvAcq, target);
             // The target is ours (INUSE): let the root go before writing it.
-            lane_unlock(1);
+            root_unlock();
         }
         pf_add(pfInsRootHold, now() - t_root);
         const unsigned long long t3 = now();
+        __syncthreads();  // nobody writes the target before the claim above
         cta_store<Key, T>(node(target), bat, K);
         count(cVisits);
         __syncthreads();
@@ -491,15 +530,19 @@ struct HeapCta {
             if (leader()) {
                 // park: others may take the slot meanwhile
                 lane_unlock(cur, kInsHold);
-                uint32_t* pp = st(parent);
-                Backoff b;
-                for (;;) {
-                    const uint32_t s = state_load(pp);
-                    if (s == kAvail && state_cas(pp, kAvail, kInUse)) break;
-                    if (s == kDelMod && state_cas(pp, kDelMod, kInUse)) break;
-                    b.pause();
+                if (parent == 1) {
+                    root_lock();
+                } else {
+                    uint32_t* pp = st(parent);
+                    Backoff b;
+                    for (;;) {
+                        const uint32_t s = state_load(pp);
+                        if (s == kAvail && state_cas(pp, kAvail, kInUse)) break;
+                        if (s == kDelMod && state_cas(pp, kDelMod, kInUse)) break;
+                        b.pause();
+                    }
+                    rec(kEvAcq, parent);
                 }
-                rec(kEvAcq, parent);
             }
             __syncthreads();
             cta_load<Key, T>(par, node(parent), K);
@@ -727,11 +770,15 @@ struct HeapCta {
         Key* R = buf(2);
         Key* sp = buf(3);
         bool pre = false;
+        const unsigned long long ta = now();
+        pf_add(pfRsHead, ta - t1);
+        unsigned long long tb = ta;
         if (last >= 4) {
             // Claim children 2 and 3 (two lanes), then the last node: the
             // same ancestor-first order as every other walk.
             acquire_children(1);
             __syncthreads();
+            tb = now();
             if (leader()) lane_claim_last(last);
             __syncthreads();
             pre = true;
@@ -742,10 +789,15 @@ struct HeapCta {
             if (leader()) lane_claim_last(last);
             __syncthreads();
         }
+        const unsigned long long tc = now();
+        pf_add(pfRsChild, tb - ta);
+        pf_add(pfRsLast, tc - tb);
         const uint32_t act = sh->act;
         cta_load<Key, T>(cur_s, node(act == kTake ? last : 1), K);
         if (plen) cta_load<Key, T>(sp, partial, plen);
         __syncthreads();
+        const unsigned long long td = now();
+        pf_add(pfRsLoad, td - tc);
         if (act == kTake) {
             cta_fill<Key, T>(node(last), kMaxKey, K);
             __syncthreads();
@@ -766,6 +818,7 @@ struct HeapCta {
             }
             __syncthreads();
         }
+        pf_add(pfRsFill, now() - td);
         heapify_down(ci, pre, t1);
         status(opi, BH_OK, K, seq);
         rec(kEvRes, 0);
@@ -803,12 +856,17 @@ struct HeapCta {
             Key* R = buf(ri);
             const unsigned long long l = 2 * cur, r = 2 * cur + 1;
             if (!pre) {
+                const unsigned long long tl0 = now();
                 acquire_children(cur);
                 __syncthreads();
+                const unsigned long long tl1 = now();
                 if (sh->lk) cta_load<Key, T>(L, node(l), K);
                 if (sh->rk) cta_load<Key, T>(R, node(r), K);
                 __syncthreads();
+                pf_add(pfLvAcq, tl1 - tl0);
+                pf_add(pfLvLoad, now() - tl1);
             }
+            const unsigned long long tl2 = now();
             pre = false;
             pf_add(pfLevels, 1);
             const uint32_t lk = sh->lk, rk = sh->rk;
@@ -874,6 +932,7 @@ struct HeapCta {
                 next_ci = nxi;
             }
             count(cVisits);
+            const unsigned long long tl3 = now();
             __syncthreads();
             const uint32_t hi_rel = hi_left ? sh->lrel : sh->rrel;
             if (leader()) {
@@ -881,6 +940,8 @@ struct HeapCta {
                 if (lo_locked) lane_unlock(lo, lo_rel);
                 lane_unlock(cur, cur_rel);
             }
+            pf_add(pfLvMerge, tl3 - tl2);
+            pf_add(pfLvRel, now() - tl3);
             if (cur == 1) pf_add(pfDelRootHold, now() - t_root);
             cur = hi;
             cur_rel = hi_rel;

@@ -20,6 +20,9 @@ enum : uint32_t {
 // One state word per 32-byte sector so lock traffic on neighbouring nodes
 // never shares an L2 atomic sector.
 constexpr uint32_t kStateStride = 8;  // uint32 words
+// Root queue lock: one flag per waiter slot, each on its own 128-byte line.
+constexpr uint32_t kRootQueue = 4096;
+constexpr uint32_t kRootFlagStride = 32;  // uint32 words
 
 // Heap header, root-lock guarded (reference heap.hpp:173-177).  One cache
 // line; the partial buffer follows in its own allocation.
@@ -31,7 +34,10 @@ struct alignas(128) Header {
     unsigned long long partial_len;
     unsigned long long error_flags;   // protocol faults seen on device
     unsigned long long clock;         // event-log clock (RECORD)
-    unsigned long long pad;
+    unsigned long long pad0[9];
+    // second line: waiters' ticket traffic stays off the holder's line
+    unsigned long long root_tail;     // root queue-lock ticket dispenser
+    unsigned long long pad1[15];
 };
 
 // Device counters (reference HeapCounters, heap.hpp:49-58).
@@ -67,6 +73,7 @@ struct DevEvent {
 struct HeapView {
     void* keys;              // slot_count * k keys; node i (1-based) at (i-1)*k
     uint32_t* states;        // (slot_count + 1) * kStateStride
+    uint32_t* root_flags;    // kRootQueue * kRootFlagStride
     Header* hdr;
     void* partial;           // k keys
     unsigned long long* counters;

@@ -61,4 +61,8 @@ for k in a.k:
                       f"del/op us: rootwait {us(p['del_root_wait'], p['del_ops']):.2f} roothold {us(p['del_root_hold'], p['del_ops']):.2f} "
                       f"heapify {us(p['del_rest'], p['del_ops']):.2f} childwait {us(p['child_wait'], p['del_ops']):.2f} "
                       f"levels/del {p['levels']/max(p['del_ops'],1):.2f}", flush=True)
+                d = p['del_ops']; lv = max(p['levels'] - d, 1)
+                print(f"   del root step us: head {us(p['rs_head'], d):.2f} child {us(p['rs_child'], d):.2f} last {us(p['rs_last'], d):.2f} "
+                      f"load {us(p['rs_load'], d):.2f} fill {us(p['rs_fill'], d):.2f} | per level us: acq {us(p['lv_acq'], lv):.2f} "
+                      f"load {us(p['lv_load'], lv):.2f} merge {us(p['lv_merge'], p['levels']):.2f} rel {us(p['lv_rel'], p['levels']):.2f}", flush=True)
             heap.close()
