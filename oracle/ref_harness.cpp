@@ -27,6 +27,7 @@
 #include "batchheap/graph.hpp"
 #include "batchheap/heap.hpp"
 #include "batchheap/knapsack.hpp"
+#include "batchheap/lincheck.hpp"
 #include "batchheap/seq_heap.hpp"
 #include "batchheap/sssp.hpp"
 #include "batchheap/workload.hpp"
@@ -205,6 +206,34 @@ int ref_run_workload(int variant, std::uint32_t k, std::uint32_t workers, std::u
         out[2] = static_cast<double>(row.counters.merges);
         out[3] = static_cast<double>(row.counters.early_stops);
         out[4] = row.mean_nodes_traversed;
+    });
+}
+
+// The reference's own concurrent stress runner (proj/src/workload.cpp:75-147)
+// plus its checkers (proj/src/lincheck.cpp).  out[0] invariants ok,
+// out[1] multiset ok, out[2] constructive check (check_td / check_bu) ok,
+// out[3] mutual exclusion ok, out[4] lock order ok, out[5] ops recorded.
+int ref_stress(int variant, std::uint32_t k, std::uint32_t workers, std::uint64_t ops_per_worker,
+               std::uint32_t partial_pct, std::uint64_t seed, std::uint64_t key_range, int elide,
+               int* out) {
+    return guarded([&] {
+        StressSpec s;
+        s.variant = variant ? Variant::BU : Variant::TD;
+        s.k = k;
+        s.workers = workers;
+        s.ops_per_worker = ops_per_worker;
+        s.partial_pct = partial_pct;
+        s.seed = seed;
+        s.key_range = key_range;
+        s.options.elide_merges = elide != 0;
+        s.watchdog_seconds = 60;
+        StressOutcome o = run_stress(s);
+        out[0] = o.invariants.ok;
+        out[1] = o.multiset_ok;
+        out[2] = (variant ? check_bu(o.history) : check_td(o.history)).pass;
+        out[3] = check_mutual_exclusion(o.history).ok;
+        out[4] = check_lock_order(o.history).ok;
+        out[5] = static_cast<int>(o.history.ops.size());
     });
 }
 

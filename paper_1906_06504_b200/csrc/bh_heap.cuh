@@ -515,7 +515,7 @@ struct HeapCta {
             }
             rec(kEvAcq, target);
             // The target is ours (INUSE): let the root go before writing it.
-            root_unlock();
+            if (!(hv.flags & kDbgWriteUnderRoot)) root_unlock();
         }
         pf_add(pfInsRootHold, now() - t_root);
         const unsigned long long t3 = now();
@@ -523,6 +523,7 @@ struct HeapCta {
         cta_store<Key, T>(node(target), bat, K);
         count(cVisits);
         __syncthreads();
+        if ((hv.flags & kDbgWriteUnderRoot) && leader()) root_unlock();
 
         unsigned long long cur = target;  // held
         while (cur != 1) {
@@ -643,6 +644,16 @@ struct HeapCta {
 
     // Claims both children of `cur` with lanes 0 and 1 of warp 0.
     __device__ void acquire_children(unsigned long long cur) {
+        if (hv.flags & kDbgSerialLanes) {
+            if (leader()) {
+                uint32_t rel;
+                sh->lk = lane_acquire_child(2 * cur, rel);
+                sh->lrel = rel;
+                sh->rk = lane_acquire_child(2 * cur + 1, rel);
+                sh->rrel = rel;
+            }
+            return;
+        }
         if (threadIdx.x < 2) {
             const unsigned long long t = now();
             uint32_t rel;
@@ -773,7 +784,7 @@ struct HeapCta {
         const unsigned long long ta = now();
         pf_add(pfRsHead, ta - t1);
         unsigned long long tb = ta;
-        if (last >= 4) {
+        if (last >= 4 && !(hv.flags & kDbgSeqRefill)) {
             // Claim children 2 and 3 (two lanes), then the last node: the
             // same ancestor-first order as every other walk.
             acquire_children(1);

@@ -24,6 +24,11 @@ constexpr uint32_t kStateStride = 8;  // uint32 words
 constexpr uint32_t kRootQueue = 4096;
 constexpr uint32_t kRootFlagStride = 32;  // uint32 words
 
+// Debug-only protocol toggles (bh_create flags, not in the public header).
+constexpr uint32_t kDbgSeqRefill = 0x100;       // reference refill order in every delete
+constexpr uint32_t kDbgWriteUnderRoot = 0x200;  // BU target written before the root release
+constexpr uint32_t kDbgSerialLanes = 0x400;     // claim children one after the other
+
 // Heap header, root-lock guarded (reference heap.hpp:173-177).  One cache
 // line; the partial buffer follows in its own allocation.
 struct alignas(128) Header {

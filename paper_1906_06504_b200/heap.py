@@ -114,10 +114,12 @@ class GeneralizedHeap:
 
     def __init__(self, variant: Variant, k: int, max_nodes: int,
                  options: Optional[HeapOptions] = None, record: bool = False,
-                 key_bits: int = 64, device: int = 0, profile: bool = False):
+                 key_bits: int = 64, device: int = 0, profile: bool = False,
+                 debug_flags: int = 0):
         options = options or HeapOptions()
         flags = (L.BH_FLAG_ELIDE_MERGES if options.elide_merges else 0) | \
-                (L.BH_FLAG_RECORD if record else 0) | (L.BH_FLAG_PROFILE if profile else 0)
+                (L.BH_FLAG_RECORD if record else 0) | (L.BH_FLAG_PROFILE if profile else 0) | \
+                int(debug_flags)
         h = C.c_void_p()
         _raise(L.lib().bh_create(C.byref(h), int(variant), int(k), int(max_nodes),
                                  int(key_bits), flags, int(device)))
