@@ -355,10 +355,17 @@ struct HeapCta {
             return;
         }
         const unsigned long long target = slot_for_rank(rank);
+        // Deviation from the reference (heap.cpp:171-186): a BU insert whose
+        // full batch absorbed partial-buffer keys keeps the root for its whole
+        // climb.  Those keys were already visible to deleters; a climb that
+        // lets the root go hides them until it finishes, and a concurrent
+        // deleteMin can then miss them (non-linearizable histories, found by
+        // the exhaustive checker; SURVEY.md section 4 has the reference's
+        // other known bug).
         if (hv.variant == BH_TD)
             insert_td(target, comb, t2);
         else
-            insert_bu(target, comb, t2);
+            insert_bu(target, comb, t2, plen > 0);
         status(opi, BH_OK, 0, seq);
         rec(kEvRes, 0);
     }
@@ -396,7 +403,10 @@ struct HeapCta {
             uint32_t* p = st(target);
             Backoff b;
             for (;;) {
-                if (state_load(p) == kAvail && state_cas(p, kAvail, kTarget)) break;
+                const uint32_t s = state_load(p);
+                if (s == kAvail && state_cas(p, kAvail, kTarget)) break;
+                // (BU heaps) a slot consumed from a parked climb
+                if (s == kDelMod && state_cas(p, kDelMod, kTarget)) break;
                 b.pause();
             }
         }
@@ -492,16 +502,19 @@ struct HeapCta {
             const uint32_t s = state_load(st(slot));
             if (s == kDelMod) {
                 if (state_cas(st(slot), kDelMod, kAvail)) return;
-            } else if (s == kAvail || s == kInsHold) {
-                return;
+            } else if (s == kAvail || s == kInsHold || s == kTarget || s == kMarked) {
+                return;  // a later insert owns the slot now
             } else {
                 b.pause();
             }
         }
     }
 
-    // insert_bu (heap.cpp:295-373).  Root held on entry.
-    __device__ void insert_bu(unsigned long long target, Key* bat, unsigned long long t_root) {
+    // insert_bu (heap.cpp:295-373).  Root held on entry.  With `hold` the
+    // root stays locked until the climb ends (see do_insert); parents parked
+    // by other climbers are then taken over (INSHOLD -> INUSE, released as
+    // DELMOD), because their owners may be queued on the root we hold.
+    __device__ void insert_bu(unsigned long long target, Key* bat, unsigned long long t_root, bool hold) {
         Key* par = bat == buf(4) ? buf(1) : buf(4);
         Key* cu = buf(5);
         if (leader()) {
@@ -515,68 +528,83 @@ struct HeapCta {
             }
             rec(kEvAcq, target);
             // The target is ours (INUSE): let the root go before writing it.
-            if (!(hv.flags & kDbgWriteUnderRoot)) root_unlock();
+            if (!hold && !(hv.flags & kDbgWriteUnderRoot)) root_unlock();
         }
-        pf_add(pfInsRootHold, now() - t_root);
+        if (!hold) pf_add(pfInsRootHold, now() - t_root);
         const unsigned long long t3 = now();
         __syncthreads();  // nobody writes the target before the claim above
         cta_store<Key, T>(node(target), bat, K);
         count(cVisits);
         __syncthreads();
-        if ((hv.flags & kDbgWriteUnderRoot) && leader()) root_unlock();
+        if (!hold && (hv.flags & kDbgWriteUnderRoot) && leader()) root_unlock();
 
         unsigned long long cur = target;  // held
         while (cur != 1) {
             const unsigned long long parent = cur >> 1;
+            // holding the root, the last step merges straight into it
+            const bool direct = hold && parent == 1;
             if (leader()) {
-                // park: others may take the slot meanwhile
-                lane_unlock(cur, kInsHold);
-                if (parent == 1) {
-                    root_lock();
-                } else {
-                    uint32_t* pp = st(parent);
-                    Backoff b;
-                    for (;;) {
-                        const uint32_t s = state_load(pp);
-                        if (s == kAvail && state_cas(pp, kAvail, kInUse)) break;
-                        if (s == kDelMod && state_cas(pp, kDelMod, kInUse)) break;
-                        b.pause();
+                uint32_t prel = kAvail;
+                if (!direct) {
+                    // park: others may take the slot meanwhile
+                    lane_unlock(cur, kInsHold);
+                    if (parent == 1) {
+                        root_lock();
+                    } else {
+                        uint32_t* pp = st(parent);
+                        Backoff b;
+                        for (;;) {
+                            const uint32_t s = state_load(pp);
+                            if (s == kAvail && state_cas(pp, kAvail, kInUse)) break;
+                            if (s == kDelMod && state_cas(pp, kDelMod, kInUse)) break;
+                            if (hold && s == kInsHold && state_cas(pp, kInsHold, kInUse)) {
+                                prel = kDelMod;
+                                break;
+                            }
+                            b.pause();
+                        }
+                        rec(kEvAcq, parent);
                     }
-                    rec(kEvAcq, parent);
                 }
+                sh->lastrel = prel;
             }
             __syncthreads();
             cta_load<Key, T>(par, node(parent), K);
+            const uint32_t prel = sh->lastrel;
             __syncthreads();
-            if (par[0] == kMaxKey) {
+            if (!direct && par[0] == kMaxKey) {
                 // parent was deleted: the subtree with our parked slot is gone
                 if (leader()) {
-                    lane_unlock(parent);
+                    lane_unlock(parent, prel);
                     lane_abandon_park(cur);
+                    if (hold && parent != 1) lane_unlock(1);
                 }
                 pf_add(pfInsRest, now() - t3);
                 return;
             }
             if (leader()) {
-                uint32_t owned = 0;
-                uint32_t* pc = st(cur);
-                Backoff b;
-                for (;;) {
-                    const uint32_t s = state_load(pc);
-                    if (s == kInsHold) {
-                        if (state_cas(pc, kInsHold, kInUse)) {
-                            owned = 1;
-                            break;
+                uint32_t owned = 1;  // direct: cur was never let go
+                if (!direct) {
+                    owned = 0;
+                    uint32_t* pc = st(cur);
+                    Backoff b;
+                    for (;;) {
+                        const uint32_t s = state_load(pc);
+                        if (s == kInsHold) {
+                            if (state_cas(pc, kInsHold, kInUse)) {
+                                owned = 1;
+                                break;
+                            }
+                        } else if (s == kDelMod) {
+                            if (state_cas(pc, kDelMod, kAvail)) break;
+                        } else if (s == kAvail || s == kTarget || s == kMarked) {
+                            break;  // consumed (and maybe re-claimed since)
+                        } else {
+                            b.pause();  // INUSE: a deleter is working on it
                         }
-                    } else if (s == kDelMod) {
-                        if (state_cas(pc, kDelMod, kAvail)) break;
-                    } else if (s == kAvail) {
-                        break;
-                    } else {
-                        b.pause();  // INUSE: a deleter is working on it
                     }
+                    if (owned) rec(kEvAcq, cur);
                 }
-                if (owned) rec(kEvAcq, cur);
                 sh->owned = owned;
             }
             __syncthreads();
@@ -589,7 +617,8 @@ struct HeapCta {
                     count(cEarlyStops);
                     if (leader()) {
                         lane_unlock(cur);
-                        lane_unlock(parent);
+                        lane_unlock(parent, prel);
+                        if (hold && parent != 1) lane_unlock(1);
                     }
                     pf_add(pfInsRest, now() - t3);
                     return;
@@ -610,6 +639,7 @@ struct HeapCta {
             cur = parent;
         }
         if (leader()) lane_unlock(1);
+        if (hold) pf_add(pfInsRootHold, now() - t_root);
         pf_add(pfInsRest, now() - t3);
     }
 
@@ -623,16 +653,19 @@ struct HeapCta {
         Backoff b;
         for (;;) {
             const uint32_t s = state_load(p);
+            // The state names its protocol: TARGET/MARKED come from top-down
+            // walks (TD heaps, and BU inserts that walk), INSHOLD/DELMOD
+            // from bottom-up climbs, so one rule set serves both variants.
             if (s == kAvail) {
                 if (state_cas(p, kAvail, kInUse)) break;
-            } else if (hv.variant == BH_TD && (s == kTarget || s == kMarked)) {
+            } else if (s == kTarget || s == kMarked) {
                 return 0;  // frozen empty while we hold the parent
-            } else if (hv.variant == BH_BU && s == kInsHold) {
+            } else if (s == kInsHold) {
                 if (state_cas(p, kInsHold, kInUse)) {
                     rel = kDelMod;
                     break;
                 }
-            } else if (hv.variant == BH_BU && s == kDelMod) {
+            } else if (s == kDelMod) {
                 if (state_cas(p, kDelMod, kInUse)) break;
             } else {
                 b.pause();
@@ -682,18 +715,18 @@ struct HeapCta {
                     act = kTake;
                     break;
                 }
-            } else if (hv.variant == BH_TD && s == kTarget) {
+            } else if (s == kTarget) {
                 if (state_cas(p, kTarget, kMarked)) {
                     act = kCoop;
                     break;
                 }
-            } else if (hv.variant == BH_BU && s == kInsHold) {
+            } else if (s == kInsHold) {
                 if (state_cas(p, kInsHold, kInUse)) {  // take the in-flight batch
                     act = kTake;
                     rel = kDelMod;
                     break;
                 }
-            } else if (hv.variant == BH_BU && s == kDelMod) {
+            } else if (s == kDelMod) {
                 if (state_cas(p, kDelMod, kInUse)) {
                     act = kTake;
                     break;

@@ -168,7 +168,10 @@ def test_linearizability_recorded(variant, key_hi):
         assert ok, why
         ok, why = LC.check_lock_order(hist)
         assert ok, why
-        res = LC.check_td(hist, k) if variant == Variant.TD else LC.check_bu(hist, k)
+        # TD: the reference's constructive order (root release).  BU: the
+        # reference's order (last-lock release), repaired for inserts whose
+        # parked batch a deleter consumed early (see oracle/lincheck.py).
+        res = LC.check_td(hist, k) if variant == Variant.TD else LC.check_bu_repaired(hist, k)
         assert res.passed, res.detail
         if variant == Variant.BU:
             ok, why = LC.check_bu_overlap_windows(hist)
@@ -180,15 +183,17 @@ def test_linearizability_recorded(variant, key_hi):
 @pytest.mark.parametrize("variant", [Variant.TD, Variant.BU])
 def test_constructive_implies_exhaustive(variant):
     """SPEC acceptance 4 analogue on small histories (<= 16 ops)."""
-    for trial in range(40):
+    for trial in range(200):
         rng = np.random.default_rng(5000 + trial)
         ops, pool, out_len, _ = mixed_ops(rng, 14, 2, 30, 12)
         heap = GeneralizedHeap(variant, 2, 32, record=True)
         r = heap.run_ops(ops, pool, out_len, ctas=4)
         hist = _recorded_history(heap, ops, r, pool)
-        res = LC.check_td(hist, 2) if variant == Variant.TD else LC.check_bu(hist, 2)
+        res = LC.check_td(hist, 2) if variant == Variant.TD else LC.check_bu_repaired(hist, 2)
+        ex = LC.check_exhaustive(hist, 2)
+        assert ex.passed, ex.detail
+        # constructive PASS must imply exhaustive PASS (it produced a witness)
         assert res.passed, res.detail
-        assert LC.check_exhaustive(hist, 2).passed
 
 
 def test_mutated_history_fails():

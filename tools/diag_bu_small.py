@@ -16,7 +16,7 @@ for variant in (Variant.BU, Variant.TD):
     for key_hi in (1 << 40, 12):
         c_fail = e_fail = rep_fail = 0
         shown = False
-        for trial in range(400):
+        for trial in range(1500):
             rng = np.random.default_rng(9000 + trial)
             ops, pool, out_len, _ = mixed_ops(rng, 16, 2, 30, key_hi)
             heap = GeneralizedHeap(variant, 2, 64, record=True)
@@ -39,5 +39,5 @@ for variant in (Variant.BU, Variant.TD):
                               f"inv={op.invoke_ts} res={op.respond_ts} acR={op.root_acquire_ts} "
                               f"reR={op.root_release_ts} acL={op.last_acquire_ts} reL={op.last_release_ts} "
                               f"locks={[(s.node, s.acquire_ts, s.release_ts) for s in op.locks]}")
-        print(f"{variant.name} key_hi={key_hi}: constructive-fail {c_fail}/400, repaired-fail {rep_fail}, "
+        print(f"{variant.name} key_hi={key_hi}: constructive-fail {c_fail}/1500, repaired-fail {rep_fail}, "
               f"exhaustive-fail {e_fail}", flush=True)
