@@ -225,6 +225,76 @@ def check_bu_repaired(history: List[OpRecord], k: int) -> CheckResult:
     return res
 
 
+def check_jit(history: List[OpRecord], k: int) -> CheckResult:
+    """Constructive checker with just-in-time insert placement.
+
+    Deletes are placed at their root release (every delete's result is the
+    root batch it held, and root windows are totally ordered).  Each insert
+    is placed as late as its window allows -- at its response -- unless a
+    delete returns one of its keys first; then it is pulled to just before
+    that delete, which needs the insert to have been invoked before the
+    delete's root release.  Every placement lies inside the op's own
+    [invocation, response] window, so the order respects real time by
+    construction; PASS comes with the witness, replayed exactly through the
+    multiset oracle, and therefore proves linearizability.  (It subsumes
+    check_td's order for TD and repairs check_bu's for BU, whose
+    last-lock-release order cannot place inserts whose parked batch a
+    deleter consumed, proj/src/heap.cpp:508-516,567-573.)"""
+    events = []
+    for op in history:
+        if op.op == DELETE:
+            events.append((op.root_release_ts, 1, op))
+        else:
+            events.append((op.respond_ts, 0, op))
+    events.sort(key=lambda e: (e[0], e[1]))
+    pending_by_key: Dict[int, List[OpRecord]] = {}
+    for op in history:
+        if op.op == INSERT:
+            for key in set(op.keys):
+                pending_by_key.setdefault(key, []).append(op)
+    for lst in pending_by_key.values():
+        lst.sort(key=lambda o: o.invoke_ts)
+    applied = set()
+    state = SortedList()
+    witness: List[OpRecord] = []
+    pulled = 0
+
+    def apply(ins):
+        applied.add(ins.opid)
+        state.update(ins.keys)
+        witness.append(ins)
+
+    for _, kind, op in events:
+        if kind == 0:
+            if op.opid not in applied:
+                apply(op)
+            continue
+        want = list(op.keys)
+        need: Dict[int, int] = {}
+        for key in want:
+            need[key] = need.get(key, 0) + 1
+        for key, cnt in need.items():
+            have = state.count(key)
+            while have < cnt:
+                cands = [c for c in pending_by_key.get(key, ())
+                         if c.opid not in applied and c.invoke_ts < op.root_release_ts]
+                if not cands:
+                    return CheckResult(False, f"{_describe(op)} returned key {key} that no insert invoked "
+                                              f"before its root release can supply")
+                apply(cands[0])
+                pulled += 1
+                have = state.count(key)
+        take = min(k, len(state))
+        got = [state.pop(0) for _ in range(take)]
+        if got != want:
+            return CheckResult(False, f"{_describe(op)} returned {want[:4]} but the oracle gives {got[:4]}")
+        witness.append(op)
+    res = replay_in_order(witness, k)
+    if res.passed:
+        res.detail = f"pulled {pulled} inserts"
+    return res
+
+
 def check_exhaustive(history: List[OpRecord], k: int) -> CheckResult:
     n = len(history)
     if n > 20:
