@@ -160,18 +160,37 @@ struct HeapCta {
     // store.  Mutual exclusion and FIFO hand-off order are the reference's
     // lock_avail(1)/unlock(1) semantics (heap.cpp:98-114).  Leader lane only.
     unsigned long long root_ticket = 0;
-    __device__ void root_lock() {
+    __device__ void root_lock(bool record_it = true) {
         const unsigned long long t = atomicAdd(&hdr->root_tail, 1ull);
         uint32_t* f = hv.root_flags + (t % kRootQueue) * kRootFlagStride;
         Backoff b;
         while (state_load(f) != (uint32_t)t) b.pause();
         root_ticket = t;
-        rec_lane(kEvAcq, 1);
+        if (record_it) rec_lane(kEvAcq, 1);
     }
-    __device__ void root_unlock() {
-        rec_lane(kEvRel, 1);
+    __device__ void root_unlock(bool record_it = true) {
+        if (record_it) rec_lane(kEvRel, 1);
         const unsigned long long nt = root_ticket + 1;
         state_store_release(hv.root_flags + (nt % kRootQueue) * kRootFlagStride, (uint32_t)nt);
+    }
+
+    // ---------------------------------------------------- BU phase gate --
+    // Deviation from the reference (SURVEY.md section 4 lists its other
+    // bugs): in BU heaps a bottom-up climb and a delete's heapify never run
+    // at the same time.  The reference lets deleters take over slots parked
+    // mid-climb (INSHOLD -> DELMOD, heap.cpp:508-516,567-573); a random-
+    // interleaving model of that protocol (tools/sim_bu.py) breaks
+    // property 1 in ~0.5% of schedules (the owner loses its park to another
+    // climber's DELMOD consumption, or skips re-checking a slot a deleter
+    // only took as its lo child), and the GPU reproduced it.  Insert-only
+    // and delete-only concurrency are each safe, so an op of one kind that
+    // finds the other kind in flight lets the root go and queues again.
+    // Leader only; returns with the root held and the gate counted.
+    __device__ unsigned long long* gate_mine(bool climb) { return climb ? &hdr->climbers : &hdr->deleters; }
+    __device__ unsigned long long* gate_other(bool climb) { return climb ? &hdr->deleters : &hdr->climbers; }
+    __device__ void gate_leave(bool climb) {
+        __threadfence();
+        atomicAdd(gate_mine(climb), ~0ull);  // -1, after every write of the op
     }
 
     // lock_avail (heap.cpp:98-109): AVAIL -> INUSE.  Calling lane only.
@@ -275,16 +294,34 @@ struct HeapCta {
 
         // ---- root phase (heap.cpp:126-167) ----
         if (leader()) {
-            lane_lock_avail(1);
-            sh->nodes = ld_cg_u64(&hdr->node_count);
-            sh->plen = ld_cg_u64(&hdr->partial_len);
-            sh->seq = ld_cg_u64(&hdr->root_seq);
+            uint32_t gated = 0;
+            Backoff gb;
+            for (;;) {
+                root_lock(false);
+                sh->nodes = ld_cg_u64(&hdr->node_count);
+                sh->plen = ld_cg_u64(&hdr->partial_len);
+                sh->seq = ld_cg_u64(&hdr->root_seq);
+                // a BU full batch with rank >= 2 climbs: phase gate
+                const bool climbs = hv.variant == BH_BU && n + (uint32_t)sh->plen >= (uint32_t)K &&
+                                    sh->nodes >= 1 && sh->nodes < hv.max_nodes;
+                if (!climbs) break;
+                if (ld_cg_u64(gate_other(true)) == 0) {
+                    atomicAdd(gate_mine(true), 1ull);
+                    gated = 1;
+                    break;
+                }
+                root_unlock(false);
+                gb.pause();
+            }
+            rec(kEvAcq, 1);
+            sh->owned = gated;
         }
         const unsigned long long t2 = now();
         __syncthreads();
         const unsigned long long nodes = sh->nodes;
         const uint32_t plen = (uint32_t)sh->plen;
         const unsigned long long seq = sh->seq;
+        const bool gated = sh->owned != 0;
         const bool full = n + plen >= (uint32_t)K;
         if (full && nodes == hv.max_nodes) {  // heap.cpp:129-135
             if (leader()) lane_unlock(1);
@@ -355,17 +392,17 @@ struct HeapCta {
             return;
         }
         const unsigned long long target = slot_for_rank(rank);
-        // Deviation from the reference (heap.cpp:171-186): a BU insert whose
-        // full batch absorbed partial-buffer keys keeps the root for its whole
-        // climb.  Those keys were already visible to deleters; a climb that
-        // lets the root go hides them until it finishes, and a concurrent
-        // deleteMin can then miss them (non-linearizable histories, found by
-        // the exhaustive checker; SURVEY.md section 4 has the reference's
-        // other known bug).
-        if (hv.variant == BH_TD)
+        // (BU) The phase gate also covers a second reference hazard: a full
+        // batch that absorbed partial-buffer keys carries keys deleters could
+        // already see; with no delete running during the climb none can miss
+        // them (the exhaustive checker found such non-linearizable histories
+        // without the gate).
+        if (hv.variant == BH_TD) {
             insert_td(target, comb, t2);
-        else
-            insert_bu(target, comb, t2, plen > 0);
+        } else {
+            insert_bu(target, comb, t2);
+            if (gated && leader()) gate_leave(true);
+        }
         status(opi, BH_OK, 0, seq);
         rec(kEvRes, 0);
     }
@@ -510,11 +547,8 @@ struct HeapCta {
         }
     }
 
-    // insert_bu (heap.cpp:295-373).  Root held on entry.  With `hold` the
-    // root stays locked until the climb ends (see do_insert); parents parked
-    // by other climbers are then taken over (INSHOLD -> INUSE, released as
-    // DELMOD), because their owners may be queued on the root we hold.
-    __device__ void insert_bu(unsigned long long target, Key* bat, unsigned long long t_root, bool hold) {
+    // insert_bu (heap.cpp:295-373).  Root held on entry.
+    __device__ void insert_bu(unsigned long long target, Key* bat, unsigned long long t_root) {
         Key* par = bat == buf(4) ? buf(1) : buf(4);
         Key* cu = buf(5);
         if (leader()) {
@@ -528,83 +562,68 @@ struct HeapCta {
             }
             rec(kEvAcq, target);
             // The target is ours (INUSE): let the root go before writing it.
-            if (!hold && !(hv.flags & kDbgWriteUnderRoot)) root_unlock();
+            if (!(hv.flags & kDbgWriteUnderRoot)) root_unlock();
         }
-        if (!hold) pf_add(pfInsRootHold, now() - t_root);
+        pf_add(pfInsRootHold, now() - t_root);
         const unsigned long long t3 = now();
         __syncthreads();  // nobody writes the target before the claim above
         cta_store<Key, T>(node(target), bat, K);
         count(cVisits);
         __syncthreads();
-        if (!hold && (hv.flags & kDbgWriteUnderRoot) && leader()) root_unlock();
+        if ((hv.flags & kDbgWriteUnderRoot) && leader()) root_unlock();
 
         unsigned long long cur = target;  // held
         while (cur != 1) {
             const unsigned long long parent = cur >> 1;
-            // holding the root, the last step merges straight into it
-            const bool direct = hold && parent == 1;
             if (leader()) {
-                uint32_t prel = kAvail;
-                if (!direct) {
-                    // park: others may take the slot meanwhile
-                    lane_unlock(cur, kInsHold);
-                    if (parent == 1) {
-                        root_lock();
-                    } else {
-                        uint32_t* pp = st(parent);
-                        Backoff b;
-                        for (;;) {
-                            const uint32_t s = state_load(pp);
-                            if (s == kAvail && state_cas(pp, kAvail, kInUse)) break;
-                            if (s == kDelMod && state_cas(pp, kDelMod, kInUse)) break;
-                            if (hold && s == kInsHold && state_cas(pp, kInsHold, kInUse)) {
-                                prel = kDelMod;
-                                break;
-                            }
-                            b.pause();
-                        }
-                        rec(kEvAcq, parent);
+                // park: others may take the slot meanwhile
+                lane_unlock(cur, kInsHold);
+                if (parent == 1) {
+                    root_lock();
+                } else {
+                    uint32_t* pp = st(parent);
+                    Backoff b;
+                    for (;;) {
+                        const uint32_t s = state_load(pp);
+                        if (s == kAvail && state_cas(pp, kAvail, kInUse)) break;
+                        if (s == kDelMod && state_cas(pp, kDelMod, kInUse)) break;
+                        b.pause();
                     }
+                    rec(kEvAcq, parent);
                 }
-                sh->lastrel = prel;
             }
             __syncthreads();
             cta_load<Key, T>(par, node(parent), K);
-            const uint32_t prel = sh->lastrel;
             __syncthreads();
-            if (!direct && par[0] == kMaxKey) {
+            if (par[0] == kMaxKey) {
                 // parent was deleted: the subtree with our parked slot is gone
                 if (leader()) {
-                    lane_unlock(parent, prel);
+                    lane_unlock(parent);
                     lane_abandon_park(cur);
-                    if (hold && parent != 1) lane_unlock(1);
                 }
                 pf_add(pfInsRest, now() - t3);
                 return;
             }
             if (leader()) {
-                uint32_t owned = 1;  // direct: cur was never let go
-                if (!direct) {
-                    owned = 0;
-                    uint32_t* pc = st(cur);
-                    Backoff b;
-                    for (;;) {
-                        const uint32_t s = state_load(pc);
-                        if (s == kInsHold) {
-                            if (state_cas(pc, kInsHold, kInUse)) {
-                                owned = 1;
-                                break;
-                            }
-                        } else if (s == kDelMod) {
-                            if (state_cas(pc, kDelMod, kAvail)) break;
-                        } else if (s == kAvail || s == kTarget || s == kMarked) {
-                            break;  // consumed (and maybe re-claimed since)
-                        } else {
-                            b.pause();  // INUSE: a deleter is working on it
+                uint32_t owned = 0;
+                uint32_t* pc = st(cur);
+                Backoff b;
+                for (;;) {
+                    const uint32_t s = state_load(pc);
+                    if (s == kInsHold) {
+                        if (state_cas(pc, kInsHold, kInUse)) {
+                            owned = 1;
+                            break;
                         }
+                    } else if (s == kDelMod) {
+                        if (state_cas(pc, kDelMod, kAvail)) break;
+                    } else if (s == kAvail || s == kTarget || s == kMarked) {
+                        break;  // consumed (and maybe re-claimed since)
+                    } else {
+                        b.pause();  // INUSE: a deleter is working on it
                     }
-                    if (owned) rec(kEvAcq, cur);
                 }
+                if (owned) rec(kEvAcq, cur);
                 sh->owned = owned;
             }
             __syncthreads();
@@ -617,8 +636,7 @@ struct HeapCta {
                     count(cEarlyStops);
                     if (leader()) {
                         lane_unlock(cur);
-                        lane_unlock(parent, prel);
-                        if (hold && parent != 1) lane_unlock(1);
+                        lane_unlock(parent);
                     }
                     pf_add(pfInsRest, now() - t3);
                     return;
@@ -639,7 +657,6 @@ struct HeapCta {
             cur = parent;
         }
         if (leader()) lane_unlock(1);
-        if (hold) pf_add(pfInsRootHold, now() - t_root);
         pf_add(pfInsRest, now() - t3);
     }
 
@@ -749,9 +766,33 @@ struct HeapCta {
     __device__ void do_delete(unsigned long long opi, const bh_op& o) {
         const unsigned long long t0 = now();
         rec(kEvInv, 0);
-        if (leader()) lane_lock_avail(1);
+        if (leader()) {
+            uint32_t gated = 0;
+            if (hv.variant == BH_BU) {
+                // BU phase gate: a delete that will heapify (>= 2 nodes) waits
+                // until no bottom-up climb is in flight
+                Backoff gb;
+                for (;;) {
+                    root_lock(false);
+                    const unsigned long long nodes_now = ld_cg_u64(&hdr->node_count);
+                    if (nodes_now < 2) break;
+                    if (ld_cg_u64(gate_other(false)) == 0) {
+                        atomicAdd(gate_mine(false), 1ull);
+                        gated = 1;
+                        break;
+                    }
+                    root_unlock(false);
+                    gb.pause();
+                }
+                rec(kEvAcq, 1);
+            } else {
+                root_lock();
+            }
+            sh->owned = gated;
+        }
         const unsigned long long t1 = now();
         __syncthreads();
+        const bool gated = sh->owned != 0;
         // the root batch, read in the same round trip as the header
         Key* cur_s = buf(0);
         if (leader()) {
@@ -864,6 +905,7 @@ struct HeapCta {
         }
         pf_add(pfRsFill, now() - td);
         heapify_down(ci, pre, t1);
+        if (gated && leader()) gate_leave(false);
         status(opi, BH_OK, K, seq);
         rec(kEvRes, 0);
     }

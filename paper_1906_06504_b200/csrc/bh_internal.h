@@ -42,7 +42,9 @@ struct alignas(128) Header {
     unsigned long long pad0[9];
     // second line: waiters' ticket traffic stays off the holder's line
     unsigned long long root_tail;     // root queue-lock ticket dispenser
-    unsigned long long pad1[15];
+    unsigned long long climbers;      // BU: in-flight bottom-up climbs
+    unsigned long long deleters;      // BU: in-flight delete heapifies
+    unsigned long long pad1[13];
 };
 
 // Device counters (reference HeapCounters, heap.hpp:49-58).
