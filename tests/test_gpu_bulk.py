@@ -168,11 +168,13 @@ def test_linearizability_recorded(variant, key_hi):
         assert ok, why
         ok, why = LC.check_lock_order(hist)
         assert ok, why
-        # TD: the reference's constructive order (root release).  BU: the
-        # reference's order (last-lock release), repaired for inserts whose
-        # parked batch a deleter consumed early (see oracle/lincheck.py).
-        res = LC.check_td(hist, k) if variant == Variant.TD else LC.check_bu_repaired(hist, k)
+        # the reference's constructive orders: TD by root release, BU by
+        # last-lock release (proj/src/lincheck.cpp:53-86) ...
+        res = LC.check_td(hist, k) if variant == Variant.TD else LC.check_bu(hist, k)
         assert res.passed, res.detail
+        # ... and the just-in-time witness builder agrees
+        jit = LC.check_jit(hist, k)
+        assert jit.passed, jit.detail
         if variant == Variant.BU:
             ok, why = LC.check_bu_overlap_windows(hist)
             assert ok, why
@@ -189,7 +191,7 @@ def test_constructive_implies_exhaustive(variant):
         heap = GeneralizedHeap(variant, 2, 32, record=True)
         r = heap.run_ops(ops, pool, out_len, ctas=4)
         hist = _recorded_history(heap, ops, r, pool)
-        res = LC.check_td(hist, 2) if variant == Variant.TD else LC.check_bu_repaired(hist, 2)
+        res = LC.check_td(hist, 2) if variant == Variant.TD else LC.check_bu(hist, 2)
         ex = LC.check_exhaustive(hist, 2)
         assert ex.passed, ex.detail
         # constructive PASS must imply exhaustive PASS (it produced a witness)
