@@ -694,7 +694,7 @@ int bh_dump(bh_heap* h, void* keys_out, uint64_t keys_cap, void* partial_out, ui
     if (states_out) {
         std::vector<uint32_t> raw((h->slot_count + 1) * kStateStride);
         BH_CUDA(cudaMemcpy(raw.data(), h->d_states, raw.size() * 4, cudaMemcpyDeviceToHost));
-        for (uint64_t i = 0; i <= h->slot_count; ++i) states_out[i] = raw[i * kStateStride];
+        for (uint64_t i = 0; i <= h->slot_count; ++i) states_out[i] = raw[i * kStateStride] & 7u;  // drop the version
     }
     return BH_OK;
 }

@@ -47,6 +47,34 @@ __device__ __forceinline__ void state_store_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Node state words carry a version above the 3-bit state: word = ver<<3 |
+// state.  Claims CAS the exact observed word (state change, same version);
+// every release bumps the version.  A claim that succeeds therefore proves
+// the node did not change between the observation and the claim, which lets
+// a CTA load a node's keys in the same round trip as the CAS that locks it.
+__device__ __forceinline__ uint32_t sget(uint32_t w) { return w & 7u; }
+__device__ __forceinline__ uint32_t swith(uint32_t w, uint32_t s) { return (w & ~7u) | s; }
+
+// Release by the holder, who knows the state it holds (`from`): one
+// red.release.gpu that bumps the version and moves the state to `to`.
+__device__ __forceinline__ void state_release(uint32_t* p, uint32_t from, uint32_t to) {
+    const uint32_t delta = 8u + to - from;
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(delta) : "memory");
+}
+
+// Warm L2 with n bytes at p (one prefetch per 128-byte line), issued by
+// threads [first, first + lines).  A hint only: the later ld.cg of the lock
+// holder reads whatever L2 holds then.
+template <int T>
+__device__ __forceinline__ void cta_prefetch_l2(const void* p, uint32_t bytes, uint32_t first) {
+    const uint32_t lines = (bytes + 127) / 128;
+    const uint32_t t = threadIdx.x - first;
+    if (threadIdx.x >= first && t < lines) {
+        const char* a = static_cast<const char*>(p) + t * 128;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
+}
+
 // Spin backoff (reference Backoff, proj/src/heap.cpp:18-31: 2^0..2^5 pause
 // rounds, then yield).  On the GPU a waiting CTA sleeps in growing steps so the
 // lock holder's SM and the contended L2 slice stay free.

@@ -13,24 +13,31 @@
 //                                  re-merge (:533-545), heapify (:547-667)
 //
 // The throughput of a lock-based heap is set by how long each op holds the
-// root (and, for deletes, each level) -- a chain of dependent L2 round trips,
-// not bandwidth.  B200-specific choices that shorten those chains (none change
-// the protocol's states, transitions or lock order):
-//   * header words and the root batch are read in the same round trip;
+// root (and, for deletes, each level): a chain of dependent L2/HBM round
+// trips, not bandwidth.  B200-specific choices that shorten the chain (none
+// changes the protocol's states, transitions or lock order):
+//   * node state words carry a version (bh_device.cuh): a node's keys are
+//     loaded in the same round trip as the CAS that claims it, and the load
+//     is kept only if the claim succeeds;
 //   * a node's two children are claimed by two lanes at once;
-//   * the delete's root refill claims children 2 and 3 first and then the
-//     last node (ancestor-before-descendant, as everywhere else), so the refill
-//     and the first heapify level share their load round trip;
+//   * the next level's children (and the delete's refill node) are
+//     prefetched into L2 while the current level merges;
+//   * the delete's refill claims children 2 and 3 before the last node
+//     (ancestor-first, as every walk) and releases the last node together
+//     with the first heapify level;
 //   * the carried batch stays in shared memory and is written back once, when
 //     its lock is released; the BU target is written after the root release
 //     (the target is already INUSE);
-//   * locks are released by one st.release.gpu after a CTA barrier (the
+//   * the root is a FIFO array queue lock (one flag line per waiter);
+//   * locks are released by one red.release.gpu after a CTA barrier (the
 //     barrier orders every thread's stores before the release);
 //   * counters are per-CTA registers folded into global memory at exit.
 //
-// Deliberate deviation: heapify's merge elision places the batch that holds
-// the smaller keys in the hi child on an equal-maxima tie (reference bug at
-// heap.cpp:628-636).
+// Deliberate deviations from the reference, each fixing a reference bug:
+//   * heapify's merge elision places the batch holding the smaller keys in
+//     the hi child on an equal-maxima tie (heap.cpp:628-636);
+//   * BU heaps run a phase gate: a bottom-up climb and a delete heapify
+//     never overlap (see gate_* below).
 #pragma once
 
 #include "bh_device.cuh"
@@ -42,8 +49,12 @@ struct OpShared {
     unsigned long long nodes;
     unsigned long long plen;
     unsigned long long seq;
+    unsigned long long deleters;
     uint32_t act;
-    uint32_t lk, rk;      // children locked?
+    uint32_t cw[3];     // observed state words (children / claimed node)
+    uint32_t claim[3];  // 1 = claimable, 0 = skip (empty)
+    uint32_t ok[3];     // CAS outcome
+    uint32_t lk, rk;    // children locked?
     uint32_t lrel, rrel;  // children release states
     uint32_t lastrel;
     uint32_t owned;
@@ -64,12 +75,12 @@ enum ProfIdx {
     pfLevels,
     pfCtaCycles,
     pfRsHead,   // delete root step: root lock -> header/root batch in smem
-    pfRsChild,  //   claim children 2 and 3
+    pfRsChild,  //   claim + load children 2 and 3
     pfRsLast,   //   claim the last node
-    pfRsLoad,   //   load children/refill/partial
-    pfRsFill,   //   sentinel-fill + release of the last node, partial re-merge
-    pfLvAcq,    // heapify level: claim children
-    pfLvLoad,   //   load children
+    pfRsLoad,   //   load the refill (+ partial)
+    pfRsFill,   //   partial re-merge
+    pfLvAcq,    // heapify level: claim + load children
+    pfLvLoad,   //   (unused: loads overlap the claims)
     pfLvMerge,  //   both merges
     pfLvRel,    //   write-back barrier + releases
     kNumProf
@@ -79,6 +90,9 @@ template <typename Key, int K, int T>
 struct HeapCta {
     static constexpr Key kMaxKey = KeyLimits<Key>::kMax;
     static constexpr int kBufs = 6;
+    static constexpr uint32_t kNodeBytes = K * sizeof(Key);
+    // prefetches are issued by warps other than the leader's
+    static constexpr uint32_t kPfFirst = T > 64 ? 64 : 0;
 
     HeapView hv;
     RunView rv;
@@ -91,6 +105,7 @@ struct HeapCta {
     unsigned long long cnt[kNumCounters];
     unsigned long long pf[kNumProf];
     unsigned long long cur_op;
+    unsigned long long root_ticket;
     bool elide;
     bool record;
     bool prof;
@@ -107,6 +122,7 @@ struct HeapCta {
         for (int i = 0; i < kNumCounters; ++i) cnt[i] = 0;
 #pragma unroll
         for (int i = 0; i < kNumProf; ++i) pf[i] = 0;
+        root_ticket = 0;
         elide = (h.flags & BH_FLAG_ELIDE_MERGES) != 0;
         record = (h.flags & BH_FLAG_RECORD) != 0;
         prof = h.prof != nullptr;
@@ -124,6 +140,11 @@ struct HeapCta {
     __device__ __forceinline__ unsigned long long now() const { return prof ? clock64() : 0ull; }
     __device__ __forceinline__ void pf_add(int idx, unsigned long long v) {
         if (prof && leader()) pf[idx] += v;
+    }
+    __device__ __forceinline__ void prefetch_node(unsigned long long slot) {
+        if (slot > hv.slot_count) return;
+        cta_prefetch_l2<T>(node(slot), kNodeBytes, kPfFirst);
+        if (threadIdx.x == kPfFirst + 32 % T) asm volatile("prefetch.global.L2 [%0];" ::"l"(st(slot)));
     }
 
     // ----------------------------------------------------------- recorder --
@@ -159,7 +180,6 @@ struct HeapCta {
     // of every CTA hammering one L2 word with CAS, and the hand-off costs one
     // store.  Mutual exclusion and FIFO hand-off order are the reference's
     // lock_avail(1)/unlock(1) semantics (heap.cpp:98-114).  Leader lane only.
-    unsigned long long root_ticket = 0;
     __device__ void root_lock(bool record_it = true) {
         const unsigned long long t = atomicAdd(&hdr->root_tail, 1ull);
         uint32_t* f = hv.root_flags + (t % kRootQueue) * kRootFlagStride;
@@ -174,49 +194,51 @@ struct HeapCta {
         state_store_release(hv.root_flags + (nt % kRootQueue) * kRootFlagStride, (uint32_t)nt);
     }
 
-    // ---------------------------------------------------- BU phase gate --
-    // Deviation from the reference (SURVEY.md section 4 lists its other
-    // bugs): in BU heaps a bottom-up climb and a delete's heapify never run
-    // at the same time.  The reference lets deleters take over slots parked
-    // mid-climb (INSHOLD -> DELMOD, heap.cpp:508-516,567-573); a random-
-    // interleaving model of that protocol (tools/sim_bu.py) breaks
-    // property 1 in ~0.5% of schedules (the owner loses its park to another
-    // climber's DELMOD consumption, or skips re-checking a slot a deleter
-    // only took as its lo child), and the GPU reproduced it.  Insert-only
-    // and delete-only concurrency are each safe, so an op of one kind that
-    // finds the other kind in flight lets the root go and queues again.
-    // Leader only; returns with the root held and the gate counted.
-    __device__ unsigned long long* gate_mine(bool climb) { return climb ? &hdr->climbers : &hdr->deleters; }
-    __device__ unsigned long long* gate_other(bool climb) { return climb ? &hdr->deleters : &hdr->climbers; }
-    __device__ void gate_leave(bool climb) {
-        __threadfence();
-        atomicAdd(gate_mine(climb), ~0ull);  // -1, after every write of the op
-    }
-
-    // lock_avail (heap.cpp:98-109): AVAIL -> INUSE.  Calling lane only.
-    __device__ void lane_lock_avail(unsigned long long slot) {
-        if (slot == 1) {
-            root_lock();
-            return;
-        }
+    // Non-root claim: wait for one of `accept` (bitmask of states), CAS it to
+    // INUSE.  Returns the state it was claimed from.  Calling lane only.
+    __device__ uint32_t lane_claim(unsigned long long slot, uint32_t accept) {
         uint32_t* p = st(slot);
         Backoff b;
         for (;;) {
-            if (state_load(p) == kAvail && state_cas(p, kAvail, kInUse)) break;
+            const uint32_t w = state_load(p);
+            if (((accept >> sget(w)) & 1u) && state_cas(p, w, swith(w, kInUse))) return sget(w);
             b.pause();
         }
-        rec_lane(kEvAcq, slot);
     }
-    // unlock (heap.cpp:111-114).  Calling lane only; the CTA has passed a
-    // barrier after its last write to data guarded by this lock, and the
-    // release store orders those writes before the state change.
+    // unlock (heap.cpp:111-114) of a node this lane's CTA holds INUSE.  The
+    // CTA has passed a barrier after its last write to the node.
     __device__ __forceinline__ void lane_unlock(unsigned long long slot, uint32_t release_as = kAvail) {
         if (slot == 1) {
             root_unlock();
             return;
         }
         rec_lane(kEvRel, slot);
-        state_store_release(st(slot), release_as);
+        state_release(st(slot), kInUse, release_as);
+    }
+
+    // ---------------------------------------------------- BU phase gate --
+    // Deviation from the reference (SURVEY.md section 4 lists its other
+    // bugs): in BU heaps a bottom-up climb and a delete's heapify never run
+    // at the same time.  The reference lets deleters take over slots parked
+    // mid-climb (INSHOLD -> DELMOD, heap.cpp:508-516,567-573); a random-
+    // interleaving model of that protocol (tools/sim_bu.py) breaks property 1
+    // in ~0.5% of schedules (the owner loses its park to another climber's
+    // DELMOD consumption, or skips re-checking a slot a deleter only took as
+    // its lo child), and the GPU reproduced it.  It also covers partial-
+    // buffer keys a full batch absorbs: visible before the climb, they would
+    // be hidden from concurrent deletes during it (non-linearizable
+    // histories, found by the exhaustive checker).  Insert-only and
+    // delete-only concurrency are each safe, so an op of one kind that finds
+    // the other kind in flight lets the root go and queues again.
+    __device__ __forceinline__ unsigned long long* gate_mine(bool climb) {
+        return climb ? &hdr->climbers : &hdr->deleters;
+    }
+    __device__ __forceinline__ unsigned long long* gate_other(bool climb) {
+        return climb ? &hdr->deleters : &hdr->climbers;
+    }
+    __device__ void gate_leave(bool climb) {
+        __threadfence();
+        atomicAdd(gate_mine(climb), ~0ull);  // -1, after every write of the op
     }
 
     __device__ void status(unsigned long long opi, uint32_t code, uint32_t len, unsigned long long seq) {
@@ -298,15 +320,19 @@ struct HeapCta {
             Backoff gb;
             for (;;) {
                 root_lock(false);
-                sh->nodes = ld_cg_u64(&hdr->node_count);
-                sh->plen = ld_cg_u64(&hdr->partial_len);
-                sh->seq = ld_cg_u64(&hdr->root_seq);
+                const unsigned long long nd = ld_cg_u64(&hdr->node_count);
+                const unsigned long long pl = ld_cg_u64(&hdr->partial_len);
+                const unsigned long long sq = ld_cg_u64(&hdr->root_seq);
+                const unsigned long long dl = hv.variant == BH_BU ? ld_cg_u64(gate_other(true)) : 0;
+                sh->nodes = nd;
+                sh->plen = pl;
+                sh->seq = sq;
                 // a BU full batch with rank >= 2 climbs: phase gate
-                const bool climbs = hv.variant == BH_BU && n + (uint32_t)sh->plen >= (uint32_t)K &&
-                                    sh->nodes >= 1 && sh->nodes < hv.max_nodes;
+                const bool climbs = hv.variant == BH_BU && n + (uint32_t)pl >= (uint32_t)K && nd >= 1 &&
+                                    nd < hv.max_nodes;
                 if (!climbs) break;
-                if (ld_cg_u64(gate_other(true)) == 0) {
-                    atomicAdd(gate_mine(true), 1ull);
+                if (dl == 0) {
+                    atomicAdd(gate_mine(true), 1ull);  // ordered before the root release
                     gated = 1;
                     break;
                 }
@@ -392,11 +418,6 @@ struct HeapCta {
             return;
         }
         const unsigned long long target = slot_for_rank(rank);
-        // (BU) The phase gate also covers a second reference hazard: a full
-        // batch that absorbed partial-buffer keys carries keys deleters could
-        // already see; with no delete running during the climb none can miss
-        // them (the exhaustive checker found such non-linearizable histories
-        // without the gate).
         if (hv.variant == BH_TD) {
             insert_td(target, comb, t2);
         } else {
@@ -435,15 +456,14 @@ struct HeapCta {
     __device__ void insert_td(unsigned long long target, Key* bat, unsigned long long t_root) {
         Key* nd = buf(4);
         Key* tmp = buf(5);
-        if (bat == buf(4)) nd = buf(1);
-        if (leader()) {  // claim the target under the root lock
+        if (leader()) {  // claim the target under the root lock: AVAIL -> TARGET
             uint32_t* p = st(target);
             Backoff b;
             for (;;) {
-                const uint32_t s = state_load(p);
-                if (s == kAvail && state_cas(p, kAvail, kTarget)) break;
-                // (BU heaps) a slot consumed from a parked climb
-                if (s == kDelMod && state_cas(p, kDelMod, kTarget)) break;
+                const uint32_t w = state_load(p);
+                const uint32_t s = sget(w);
+                // (DELMOD: BU heaps only; never seen in TD heaps)
+                if ((s == kAvail || s == kDelMod) && state_cas(p, w, swith(w, kTarget))) break;
                 b.pause();
             }
         }
@@ -454,22 +474,22 @@ struct HeapCta {
         unsigned long long cur = 1;
         const int depth = (int)level_of(target);
         enum { kShip = 1, kWrite = 2, kSkip = 3, kMerge = 4 };
-        for (int lvl = depth - 1; lvl >= 0; --lvl) {
+        for (int lvl = depth - 1; lvl >= 0;) {
             const unsigned long long next = target >> lvl;
             if (leader()) {
                 uint32_t act = 0;
-                if (cur != 1 && state_load(st(target)) == kMarked) {
+                if (cur != 1 && sget(state_load(st(target))) == kMarked) {
                     act = kShip;
                 } else if (next == target) {
                     Backoff b;
                     for (;;) {
-                        const uint32_t s = state_load(st(target));
-                        if (s == kTarget) {
-                            if (state_cas(st(target), kTarget, kInUse)) {
+                        const uint32_t w = state_load(st(target));
+                        if (sget(w) == kTarget) {
+                            if (state_cas(st(target), w, swith(w, kInUse))) {
                                 act = kWrite;
                                 break;
                             }
-                        } else if (s == kMarked) {
+                        } else if (sget(w) == kMarked) {
                             act = kShip;
                             break;
                         } else {
@@ -479,12 +499,12 @@ struct HeapCta {
                 } else {
                     Backoff b;
                     for (;;) {
-                        const uint32_t s = state_load(st(next));
+                        const uint32_t w = state_load(st(next));
+                        const uint32_t s = sget(w);
                         if (s == kAvail) {
-                            if (state_cas(st(next), kAvail, kInUse)) {
-                                act = kMerge;
-                                break;
-                            }
+                            act = kMerge;  // claimed below, overlapped with the load
+                            sh->cw[0] = w;
+                            break;
                         } else if (s == kTarget || s == kMarked) {
                             act = kSkip;  // frozen empty while we hold its ancestor
                             break;
@@ -502,7 +522,7 @@ struct HeapCta {
                 count(cCoop);
                 __syncthreads();
                 if (leader()) {
-                    state_store_release(st(target), kAvail);
+                    state_release(st(target), kMarked, kAvail);
                     lane_unlock(cur);
                 }
                 if (cur == 1) pf_add(pfInsRootHold, now() - t_root);
@@ -520,27 +540,39 @@ struct HeapCta {
                 if (leader()) lane_unlock(target);
                 return;
             }
-            if (act == kSkip) continue;
-            if (leader()) rec(kEvAcq, next);
+            if (act == kSkip) {
+                --lvl;
+                continue;
+            }
+            // kMerge: load the node while the leader's CAS claims it
             cta_load<Key, T>(nd, node(next), K);
+            if (leader()) {
+                const uint32_t w = sh->cw[0];
+                sh->ok[0] = state_cas(st(next), w, swith(w, kInUse));
+            }
             __syncthreads();
+            if (!sh->ok[0]) continue;  // lost the race: decide again
+            if (leader()) rec(kEvAcq, next);
             merge_step_down(bat, nd, tmp, next);
             count(cVisits);
             if (leader()) lane_unlock(cur);
             if (cur == 1) pf_add(pfInsRootHold, now() - t_root);
             cur = next;
+            --lvl;
         }
     }
 
     // abandon_park (heap.cpp:393-407).  Calling lane only.
     __device__ void lane_abandon_park(unsigned long long slot) {
         Backoff b;
+        uint32_t* p = st(slot);
         for (;;) {
-            const uint32_t s = state_load(st(slot));
+            const uint32_t w = state_load(p);
+            const uint32_t s = sget(w);
             if (s == kDelMod) {
-                if (state_cas(st(slot), kDelMod, kAvail)) return;
-            } else if (s == kAvail || s == kInsHold || s == kTarget || s == kMarked) {
-                return;  // a later insert owns the slot now
+                if (state_cas(p, w, swith(w, kAvail) + 8u)) return;
+            } else if (s != kInUse) {
+                return;  // AVAIL, or a later insert owns the slot now
             } else {
                 b.pause();
             }
@@ -552,17 +584,10 @@ struct HeapCta {
         Key* par = bat == buf(4) ? buf(1) : buf(4);
         Key* cu = buf(5);
         if (leader()) {
-            uint32_t* p = st(target);
-            Backoff b;
-            for (;;) {
-                const uint32_t s = state_load(p);
-                if (s == kAvail && state_cas(p, kAvail, kInUse)) break;
-                if (s == kDelMod && state_cas(p, kDelMod, kInUse)) break;
-                b.pause();
-            }
+            lane_claim(target, (1u << kAvail) | (1u << kDelMod));
             rec(kEvAcq, target);
             // The target is ours (INUSE): let the root go before writing it.
-            if (!(hv.flags & kDbgWriteUnderRoot)) root_unlock();
+            root_unlock();
         }
         pf_add(pfInsRootHold, now() - t_root);
         const unsigned long long t3 = now();
@@ -570,31 +595,40 @@ struct HeapCta {
         cta_store<Key, T>(node(target), bat, K);
         count(cVisits);
         __syncthreads();
-        if ((hv.flags & kDbgWriteUnderRoot) && leader()) root_unlock();
 
         unsigned long long cur = target;  // held
         while (cur != 1) {
             const unsigned long long parent = cur >> 1;
-            if (leader()) {
-                // park: others may take the slot meanwhile
-                lane_unlock(cur, kInsHold);
-                if (parent == 1) {
-                    root_lock();
-                } else {
-                    uint32_t* pp = st(parent);
-                    Backoff b;
-                    for (;;) {
-                        const uint32_t s = state_load(pp);
-                        if (s == kAvail && state_cas(pp, kAvail, kInUse)) break;
-                        if (s == kDelMod && state_cas(pp, kDelMod, kInUse)) break;
-                        b.pause();
+            // ---- park, then claim the parent with its keys in flight ----
+            if (leader()) lane_unlock(cur, kInsHold);
+            for (;;) {
+                if (leader()) {
+                    if (parent == 1) {
+                        root_lock();
+                        sh->ok[0] = 2;  // held, nothing to validate
+                    } else {
+                        uint32_t* pp = st(parent);
+                        Backoff b;
+                        uint32_t w;
+                        for (;;) {
+                            w = state_load(pp);
+                            if (sget(w) == kAvail || sget(w) == kDelMod) break;
+                            b.pause();
+                        }
+                        sh->cw[0] = w;
+                        sh->ok[0] = 0;
                     }
-                    rec(kEvAcq, parent);
                 }
+                __syncthreads();
+                cta_load<Key, T>(par, node(parent), K);
+                if (leader() && sh->ok[0] == 0) {
+                    const uint32_t w = sh->cw[0];
+                    sh->ok[0] = state_cas(st(parent), w, swith(w, kInUse));
+                }
+                __syncthreads();
+                if (sh->ok[0]) break;
             }
-            __syncthreads();
-            cta_load<Key, T>(par, node(parent), K);
-            __syncthreads();
+            if (parent != 1 && leader()) rec(kEvAcq, parent);
             if (par[0] == kMaxKey) {
                 // parent was deleted: the subtree with our parked slot is gone
                 if (leader()) {
@@ -604,34 +638,41 @@ struct HeapCta {
                 pf_add(pfInsRest, now() - t3);
                 return;
             }
-            if (leader()) {
-                uint32_t owned = 0;
-                uint32_t* pc = st(cur);
-                Backoff b;
-                for (;;) {
-                    const uint32_t s = state_load(pc);
-                    if (s == kInsHold) {
-                        if (state_cas(pc, kInsHold, kInUse)) {
-                            owned = 1;
+            // ---- re-take the parked slot; its keys load with the CAS ----
+            for (;;) {
+                if (leader()) {
+                    uint32_t* pc = st(cur);
+                    Backoff b;
+                    uint32_t owned = 0;
+                    for (;;) {
+                        const uint32_t w = state_load(pc);
+                        const uint32_t s = sget(w);
+                        if (s == kInsHold) {
+                            sh->cw[1] = w;
+                            owned = 1;  // provisional: validated by the CAS
                             break;
+                        } else if (s == kDelMod) {
+                            if (state_cas(pc, w, swith(w, kAvail) + 8u)) break;
+                        } else if (s != kInUse) {
+                            break;  // AVAIL (or re-claimed): consumed
+                        } else {
+                            b.pause();  // INUSE: a deleter is working on it
                         }
-                    } else if (s == kDelMod) {
-                        if (state_cas(pc, kDelMod, kAvail)) break;
-                    } else if (s == kAvail || s == kTarget || s == kMarked) {
-                        break;  // consumed (and maybe re-claimed since)
-                    } else {
-                        b.pause();  // INUSE: a deleter is working on it
                     }
+                    sh->owned = owned;
                 }
-                if (owned) rec(kEvAcq, cur);
-                sh->owned = owned;
-            }
-            __syncthreads();
-            if (sh->owned) {
-                // The parked slot may have been consumed and re-claimed by a
-                // later insert (see heap.cpp:393-407), so re-read it.
-                cta_load<Key, T>(cu, node(cur), K);
                 __syncthreads();
+                if (!sh->owned) break;
+                cta_load<Key, T>(cu, node(cur), K);
+                if (leader()) {
+                    const uint32_t w = sh->cw[1];
+                    sh->ok[1] = state_cas(st(cur), w, swith(w, kInUse));
+                }
+                __syncthreads();
+                if (sh->ok[1]) break;
+            }
+            if (sh->owned) {
+                if (leader()) rec(kEvAcq, cur);
                 if (cu[0] >= par[K - 1]) {
                     count(cEarlyStops);
                     if (leader()) {
@@ -661,91 +702,98 @@ struct HeapCta {
     }
 
     // ============================================================ delete ==
-    // acquire_child (heap.cpp:547-585).  Calling lane only.  Returns
-    // locked?; rel = state to release with.
-    __device__ uint32_t lane_acquire_child(unsigned long long slot, uint32_t& rel) {
-        rel = kAvail;
-        if (slot > hv.slot_count) return 0;
-        uint32_t* p = st(slot);
-        Backoff b;
-        for (;;) {
-            const uint32_t s = state_load(p);
-            // The state names its protocol: TARGET/MARKED come from top-down
-            // walks (TD heaps, and BU inserts that walk), INSHOLD/DELMOD
-            // from bottom-up climbs, so one rule set serves both variants.
-            if (s == kAvail) {
-                if (state_cas(p, kAvail, kInUse)) break;
-            } else if (s == kTarget || s == kMarked) {
-                return 0;  // frozen empty while we hold the parent
-            } else if (s == kInsHold) {
-                if (state_cas(p, kInsHold, kInUse)) {
-                    rel = kDelMod;
-                    break;
-                }
-            } else if (s == kDelMod) {
-                if (state_cas(p, kDelMod, kInUse)) break;
-            } else {
-                b.pause();
-            }
-        }
-        rec_lane(kEvAcq, slot);
-        return 1;
-    }
-
-    // Claims both children of `cur` with lanes 0 and 1 of warp 0.
-    __device__ void acquire_children(unsigned long long cur) {
-        if (hv.flags & kDbgSerialLanes) {
-            if (leader()) {
-                uint32_t rel;
-                sh->lk = lane_acquire_child(2 * cur, rel);
-                sh->lrel = rel;
-                sh->rk = lane_acquire_child(2 * cur + 1, rel);
-                sh->rrel = rel;
-            }
-            return;
-        }
+    // Claims the children of `cur` (acquire_child, heap.cpp:547-585) with
+    // lanes 0 and 1 and loads their keys into L/R in the same round trip as
+    // the claiming CAS.  TARGET/MARKED children are frozen empty (skipped);
+    // INSHOLD children are taken over and released as DELMOD.  Sets
+    // sh->lk/rk and sh->lrel/rrel.  Ends with a barrier.
+    __device__ void acquire_children(unsigned long long cur, Key* L, Key* R) {
+        uint32_t pending = 3u;
         if (threadIdx.x < 2) {
-            const unsigned long long t = now();
-            uint32_t rel;
-            const uint32_t got = lane_acquire_child(2 * cur + threadIdx.x, rel);
             if (threadIdx.x == 0) {
-                sh->lk = got;
-                sh->lrel = rel;
-                if (prof) pf[pfChildWait] += clock64() - t;
+                sh->lk = 0;
+                sh->lrel = kAvail;
             } else {
-                sh->rk = got;
-                sh->rrel = rel;
+                sh->rk = 0;
+                sh->rrel = kAvail;
             }
         }
+        const unsigned long long t = now();
+        for (;;) {
+            if (threadIdx.x < 2 && ((pending >> threadIdx.x) & 1u)) {
+                const unsigned long long slot = 2 * cur + threadIdx.x;
+                uint32_t claim = 0, w = 0;
+                if (slot <= hv.slot_count) {
+                    uint32_t* p = st(slot);
+                    Backoff b;
+                    for (;;) {
+                        w = state_load(p);
+                        const uint32_t s = sget(w);
+                        if (s == kAvail || s == kInsHold || s == kDelMod) {
+                            claim = 1;
+                            break;
+                        }
+                        if (s == kTarget || s == kMarked) break;  // frozen empty
+                        b.pause();
+                    }
+                }
+                sh->claim[threadIdx.x] = claim;
+                sh->cw[threadIdx.x] = w;
+            }
+            __syncthreads();
+            const uint32_t cl = ((pending & 1u) && sh->claim[0]) | (((pending & 2u) && sh->claim[1]) << 1);
+            if (cl & 1u) cta_load<Key, T>(L, node(2 * cur), K);
+            if (cl & 2u) cta_load<Key, T>(R, node(2 * cur + 1), K);
+            if (threadIdx.x < 2 && ((cl >> threadIdx.x) & 1u)) {
+                const unsigned long long slot = 2 * cur + threadIdx.x;
+                const uint32_t w = sh->cw[threadIdx.x];
+                const uint32_t ok = state_cas(st(slot), w, swith(w, kInUse));
+                sh->ok[threadIdx.x] = ok;
+                if (ok) {
+                    rec_lane(kEvAcq, slot);
+                    const uint32_t rel = sget(w) == kInsHold ? kDelMod : kAvail;
+                    if (threadIdx.x == 0) {
+                        sh->lk = 1;
+                        sh->lrel = rel;
+                    } else {
+                        sh->rk = 1;
+                        sh->rrel = rel;
+                    }
+                }
+            }
+            __syncthreads();
+            uint32_t still = 0;
+            if ((cl & 1u) && !sh->ok[0]) still |= 1u;
+            if ((cl & 2u) && !sh->ok[1]) still |= 2u;
+            pending = still;
+            if (!pending) break;
+        }
+        pf_add(pfChildWait, now() - t);
     }
 
-    // refill_root_from(last) claim (heap.cpp:467-531).  Calling lane only.
+    // refill_root_from(last) claim (heap.cpp:467-531).  Leader only.
     enum { kTake = 1, kCoop = 2 };
     __device__ void lane_claim_last(unsigned long long last) {
         uint32_t* p = st(last);
         uint32_t act = 0, rel = kAvail;
         Backoff b;
         for (;;) {
-            const uint32_t s = state_load(p);
-            if (s == kAvail) {
-                if (state_cas(p, kAvail, kInUse)) {
+            const uint32_t w = state_load(p);
+            const uint32_t s = sget(w);
+            if (s == kAvail || s == kDelMod) {
+                if (state_cas(p, w, swith(w, kInUse))) {
                     act = kTake;
                     break;
                 }
             } else if (s == kTarget) {
-                if (state_cas(p, kTarget, kMarked)) {
+                if (state_cas(p, w, swith(w, kMarked))) {
                     act = kCoop;
                     break;
                 }
             } else if (s == kInsHold) {
-                if (state_cas(p, kInsHold, kInUse)) {  // take the in-flight batch
+                if (state_cas(p, w, swith(w, kInUse))) {  // take the in-flight batch
                     act = kTake;
                     rel = kDelMod;
-                    break;
-                }
-            } else if (s == kDelMod) {
-                if (state_cas(p, kDelMod, kInUse)) {
-                    act = kTake;
                     break;
                 }
             } else {
@@ -755,7 +803,7 @@ struct HeapCta {
         if (act == kCoop) {
             // the inserter ships its batch into the root, then AVAIL
             Backoff w;
-            while (state_load(p) != kAvail) w.pause();
+            while (sget(state_load(p)) != kAvail) w.pause();
         } else {
             rec_lane(kEvAcq, last);
         }
@@ -775,8 +823,9 @@ struct HeapCta {
                 for (;;) {
                     root_lock(false);
                     const unsigned long long nodes_now = ld_cg_u64(&hdr->node_count);
+                    const unsigned long long climbers = ld_cg_u64(gate_other(false));
                     if (nodes_now < 2) break;
-                    if (ld_cg_u64(gate_other(false)) == 0) {
+                    if (climbers == 0) {
                         atomicAdd(gate_mine(false), 1ull);
                         gated = 1;
                         break;
@@ -847,10 +896,12 @@ struct HeapCta {
             pf_add(pfDelRootHold, now() - t1);
             status(opi, BH_OK, K, seq);
             rec(kEvRes, 0);
+            if (gated && leader()) gate_leave(false);
             return;
         }
 
         const unsigned long long last = slot_for_rank(nodes);
+        prefetch_node(last);
         Key* L = buf(1);
         Key* R = buf(2);
         Key* sp = buf(3);
@@ -858,22 +909,18 @@ struct HeapCta {
         const unsigned long long ta = now();
         pf_add(pfRsHead, ta - t1);
         unsigned long long tb = ta;
-        if (last >= 4 && !(hv.flags & kDbgSeqRefill)) {
-            // Claim children 2 and 3 (two lanes), then the last node: the
-            // same ancestor-first order as every other walk.
-            acquire_children(1);
-            __syncthreads();
+        if (last >= 4) {
+            // Children 2 and 3 (two lanes, keys loaded with the claims), then
+            // the last node: the same ancestor-first order as every walk.
+            acquire_children(1, L, R);
             tb = now();
             if (leader()) lane_claim_last(last);
-            __syncthreads();
             pre = true;
-            if (sh->lk) cta_load<Key, T>(L, node(2), K);
-            if (sh->rk) cta_load<Key, T>(R, node(3), K);
         } else {
             __syncthreads();
             if (leader()) lane_claim_last(last);
-            __syncthreads();
         }
+        __syncthreads();
         const unsigned long long tc = now();
         pf_add(pfRsChild, tb - ta);
         pf_add(pfRsLast, tc - tb);
@@ -883,10 +930,15 @@ struct HeapCta {
         __syncthreads();
         const unsigned long long td = now();
         pf_add(pfRsLoad, td - tc);
+        unsigned long long extra = 0;  // `last`, released with the first level
         if (act == kTake) {
             cta_fill<Key, T>(node(last), kMaxKey, K);
-            __syncthreads();
-            if (leader()) lane_unlock(last, sh->lastrel);
+            if (pre) {
+                extra = last;
+            } else {
+                __syncthreads();
+                if (leader()) lane_unlock(last, sh->lastrel);
+            }
         }
 
         // ---- remerge_root_with_partial (heap.cpp:533-545) ----
@@ -904,7 +956,7 @@ struct HeapCta {
             __syncthreads();
         }
         pf_add(pfRsFill, now() - td);
-        heapify_down(ci, pre, t1);
+        heapify_down(ci, pre, t1, extra, sh->lastrel);
         if (gated && leader()) gate_leave(false);
         status(opi, BH_OK, K, seq);
         rec(kEvRes, 0);
@@ -912,8 +964,11 @@ struct HeapCta {
 
     // heapify_down (heap.cpp:591-667) with the carried batch in buf(ci).
     // Root held on entry; with `pre`, the root's children were claimed and
-    // loaded into buf(1)/buf(2) by the caller.  Releases every lock it holds.
-    __device__ void heapify_down(int ci, bool pre, unsigned long long t_root) {
+    // loaded into buf(1)/buf(2) by the caller, and `extra` (the refill's
+    // last node, if nonzero) is released with the first level.  Releases
+    // every lock it holds.
+    __device__ void heapify_down(int ci, bool pre, unsigned long long t_root, unsigned long long extra,
+                                 uint32_t extra_rel) {
         unsigned long long cur = 1;
         uint32_t cur_rel = kAvail;
         const unsigned long long t_start = now();
@@ -943,14 +998,8 @@ struct HeapCta {
             const unsigned long long l = 2 * cur, r = 2 * cur + 1;
             if (!pre) {
                 const unsigned long long tl0 = now();
-                acquire_children(cur);
-                __syncthreads();
-                const unsigned long long tl1 = now();
-                if (sh->lk) cta_load<Key, T>(L, node(l), K);
-                if (sh->rk) cta_load<Key, T>(R, node(r), K);
-                __syncthreads();
-                pf_add(pfLvAcq, tl1 - tl0);
-                pf_add(pfLvLoad, now() - tl1);
+                acquire_children(cur, L, R);
+                pf_add(pfLvAcq, now() - tl0);
             }
             const unsigned long long tl2 = now();
             pre = false;
@@ -972,6 +1021,7 @@ struct HeapCta {
                 cta_store<Key, T>(node(cur), cur_s, K);
                 __syncthreads();
                 if (leader()) {
+                    if (extra) lane_unlock(extra, extra_rel);
                     if (lk) lane_unlock(l, sh->lrel);
                     if (rk) lane_unlock(r, sh->rrel);
                     lane_unlock(cur, cur_rel);
@@ -983,27 +1033,31 @@ struct HeapCta {
             // Merge the children: lo lands in the child whose max was larger
             // (right on ties), hi in the other, which we descend into.
             bool hi_left;
-            Key* hdata;
+            bool merge_children = false;
             if (lempty) {
                 hi_left = false;
-                hdata = R;
             } else if (rempty) {
                 hi_left = true;
-                hdata = L;
             } else if (elide && !needs_merge_full<Key, K>(L, R)) {
                 count(cElided);
                 // fix of heap.cpp:628-636: the batch with the smaller keys is hi
                 hi_left = L[K - 1] <= R[0];
-                hdata = hi_left ? L : R;
             } else {
                 hi_left = !(L[K - 1] > R[K - 1]);
+                merge_children = true;
+            }
+            const unsigned long long hi = hi_left ? l : r;
+            // warm L2 with the next level while this one merges
+            prefetch_node(2 * hi);
+            prefetch_node(2 * hi + 1);
+            Key* hdata = hi_left ? L : R;
+            if (merge_children) {
                 Key* H = buf(hx);
                 cta_merge_full<Key, K, T>(L, R, H, node(hi_left ? r : l));
                 count(cMerges);
                 __syncthreads();
                 hdata = H;
             }
-            const unsigned long long hi = hi_left ? l : r;
             const unsigned long long lo = hi_left ? r : l;
             const uint32_t lo_locked = hi_left ? rk : lk;
             int next_ci;
@@ -1023,9 +1077,11 @@ struct HeapCta {
             const uint32_t hi_rel = hi_left ? sh->lrel : sh->rrel;
             if (leader()) {
                 const uint32_t lo_rel = hi_left ? sh->rrel : sh->lrel;
+                if (extra) lane_unlock(extra, extra_rel);
                 if (lo_locked) lane_unlock(lo, lo_rel);
                 lane_unlock(cur, cur_rel);
             }
+            extra = 0;
             pf_add(pfLvMerge, tl3 - tl2);
             pf_add(pfLvRel, now() - tl3);
             if (cur == 1) pf_add(pfDelRootHold, now() - t_root);

@@ -60,7 +60,7 @@ __global__ void check_kernel(HeapView hv, unsigned long long* result) {
          slot <= hv.slot_count; slot += warps) {
         uint32_t bad = 0;
         const Key* nd = keys + (slot - 1) * k;
-        if (lane == 0 && hv.states[slot * kStateStride] != kAvail) bad |= 1;
+        if (lane == 0 && (hv.states[slot * kStateStride] & 7u) != kAvail) bad |= 1;
         const bool occupied = rank_for_slot(slot) <= nodes;
         if (!occupied) {
             if (lane == 0 && nd[0] != kMax) bad |= 2;
