@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbatchheap_b200.so")
+LIB_PATH = os.environ.get("BH_LIB") or os.path.join(HERE, "libbatchheap_b200.so")
 
 BH_OK, BH_E_CONFIG, BH_E_CAPACITY, BH_E_EMPTY, BH_E_INVALID_KEY, BH_E_CUDA, BH_E_INTERNAL = range(7)
 BH_TD, BH_BU = 0, 1

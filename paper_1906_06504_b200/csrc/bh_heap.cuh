@@ -1101,9 +1101,18 @@ __global__ void __launch_bounds__(T) heap_ops_kernel(HeapView hv, RunView rv) {
     cta.run();
 }
 
+#ifndef BH_THREADS_CAP
+#define BH_THREADS_CAP 512
+#endif
+#ifndef BH_THREADS_DIV
+#define BH_THREADS_DIV 2
+#endif
+// One CTA per op: K/2 threads (two merge outputs per thread per 2K-merge),
+// capped; both knobs are build-time for tuning sweeps.
 template <typename Key, int K>
 struct KernelCfg {
-    static constexpr int kThreads = K / 2 < 32 ? 32 : (K / 2 > 512 ? 512 : K / 2);
+    static constexpr int kWant = K / BH_THREADS_DIV;
+    static constexpr int kThreads = kWant < 32 ? 32 : (kWant > BH_THREADS_CAP ? BH_THREADS_CAP : kWant);
     static constexpr uint32_t kSmem = 6u * K * sizeof(Key);
 };
 
