@@ -771,44 +771,33 @@ struct HeapCta {
         pf_add(pfChildWait, now() - t);
     }
 
-    // refill_root_from(last) claim (heap.cpp:467-531).  Leader only.
+    // refill_root_from(last) (heap.cpp:467-531), first half.  Leader only.
+    // kTake: the last node is claimable from the observed word sh->cw[2]
+    // (the caller CASes it while the CTA loads its keys); AVAIL/DELMOD
+    // release as AVAIL, an INSHOLD in-flight batch releases as DELMOD.
+    // kCoop (TD): TARGET -> MARKED, then wait until the inserter has shipped
+    // its batch into the root and set the target AVAIL.
     enum { kTake = 1, kCoop = 2 };
-    __device__ void lane_claim_last(unsigned long long last) {
+    __device__ void lane_poll_last(unsigned long long last) {
         uint32_t* p = st(last);
-        uint32_t act = 0, rel = kAvail;
         Backoff b;
         for (;;) {
             const uint32_t w = state_load(p);
             const uint32_t s = sget(w);
-            if (s == kAvail || s == kDelMod) {
-                if (state_cas(p, w, swith(w, kInUse))) {
-                    act = kTake;
-                    break;
-                }
-            } else if (s == kTarget) {
-                if (state_cas(p, w, swith(w, kMarked))) {
-                    act = kCoop;
-                    break;
-                }
-            } else if (s == kInsHold) {
-                if (state_cas(p, w, swith(w, kInUse))) {  // take the in-flight batch
-                    act = kTake;
-                    rel = kDelMod;
-                    break;
-                }
-            } else {
-                b.pause();
+            if (s == kAvail || s == kDelMod || s == kInsHold) {
+                sh->cw[2] = w;
+                sh->act = kTake;
+                sh->lastrel = s == kInsHold ? kDelMod : kAvail;
+                return;
             }
+            if (s == kTarget && state_cas(p, w, swith(w, kMarked))) {
+                Backoff wb;
+                while (sget(state_load(p)) != kAvail) wb.pause();
+                sh->act = kCoop;
+                return;
+            }
+            b.pause();
         }
-        if (act == kCoop) {
-            // the inserter ships its batch into the root, then AVAIL
-            Backoff w;
-            while (sget(state_load(p)) != kAvail) w.pause();
-        } else {
-            rec_lane(kEvAcq, last);
-        }
-        sh->act = act;
-        sh->lastrel = rel;
     }
 
     __device__ void do_delete(unsigned long long opi, const bh_op& o) {
@@ -900,46 +889,40 @@ struct HeapCta {
             return;
         }
 
+        // ---- refill_root_from(last) (heap.cpp:467-531) in the reference's
+        // order: only the root is held while the last node is claimed, so the
+        // refill overlaps the wait for the predecessor still working on
+        // level 1, and its keys load in the same round trip as the claim ----
         const unsigned long long last = slot_for_rank(nodes);
-        prefetch_node(last);
-        Key* L = buf(1);
-        Key* R = buf(2);
         Key* sp = buf(3);
-        bool pre = false;
         const unsigned long long ta = now();
         pf_add(pfRsHead, ta - t1);
-        unsigned long long tb = ta;
-        if (last >= 4) {
-            // Children 2 and 3 (two lanes, keys loaded with the claims), then
-            // the last node: the same ancestor-first order as every walk.
-            acquire_children(1, L, R);
-            tb = now();
-            if (leader()) lane_claim_last(last);
-            pre = true;
-        } else {
-            __syncthreads();
-            if (leader()) lane_claim_last(last);
-        }
-        __syncthreads();
-        const unsigned long long tc = now();
-        pf_add(pfRsChild, tb - ta);
-        pf_add(pfRsLast, tc - tb);
-        const uint32_t act = sh->act;
-        cta_load<Key, T>(cur_s, node(act == kTake ? last : 1), K);
         if (plen) cta_load<Key, T>(sp, partial, plen);
-        __syncthreads();
-        const unsigned long long td = now();
-        pf_add(pfRsLoad, td - tc);
-        unsigned long long extra = 0;  // `last`, released with the first level
-        if (act == kTake) {
-            cta_fill<Key, T>(node(last), kMaxKey, K);
-            if (pre) {
-                extra = last;
-            } else {
+        for (;;) {
+            if (leader()) lane_poll_last(last);
+            __syncthreads();
+            const uint32_t act = sh->act;
+            cta_load<Key, T>(cur_s, node(act == kTake ? last : 1), K);
+            if (act == kCoop) {
+                __syncthreads();
+                break;
+            }
+            if (leader()) {
+                const uint32_t w = sh->cw[2];
+                const uint32_t ok = state_cas(st(last), w, swith(w, kInUse));
+                sh->ok[2] = ok;
+                if (ok) rec_lane(kEvAcq, last);
+            }
+            __syncthreads();
+            if (sh->ok[2]) {
+                cta_fill<Key, T>(node(last), kMaxKey, K);
                 __syncthreads();
                 if (leader()) lane_unlock(last, sh->lastrel);
+                break;
             }
         }
+        const unsigned long long td = now();
+        pf_add(pfRsLast, td - ta);
 
         // ---- remerge_root_with_partial (heap.cpp:533-545) ----
         int ci = 0;
@@ -956,53 +939,31 @@ struct HeapCta {
             __syncthreads();
         }
         pf_add(pfRsFill, now() - td);
-        heapify_down(ci, pre, t1, extra, sh->lastrel);
+        heapify_down(ci, t1);
         if (gated && leader()) gate_leave(false);
         status(opi, BH_OK, K, seq);
         rec(kEvRes, 0);
     }
 
     // heapify_down (heap.cpp:591-667) with the carried batch in buf(ci).
-    // Root held on entry; with `pre`, the root's children were claimed and
-    // loaded into buf(1)/buf(2) by the caller, and `extra` (the refill's
-    // last node, if nonzero) is released with the first level.  Releases
-    // every lock it holds.
-    __device__ void heapify_down(int ci, bool pre, unsigned long long t_root, unsigned long long extra,
-                                 uint32_t extra_rel) {
+    // Root held on entry.  Releases every lock it holds.
+    __device__ void heapify_down(int ci, unsigned long long t_root) {
         unsigned long long cur = 1;
         uint32_t cur_rel = kAvail;
         const unsigned long long t_start = now();
         for (;;) {
             // buffer plan: L, R, H, NX distinct from the carried batch
-            int li, ri, hx, nxi;
-            if (pre) {
-                li = 1;
-                ri = 2;
-                int f[3], nf = 0;
-                for (int i = 0; i < kBufs && nf < 3; ++i)
-                    if (i != ci && i != 1 && i != 2) f[nf++] = i;
-                hx = f[0];
-                nxi = f[1];
-            } else {
-                int f[4], nf = 0;
-                for (int i = 0; i < kBufs && nf < 4; ++i)
-                    if (i != ci) f[nf++] = i;
-                li = f[0];
-                ri = f[1];
-                hx = f[2];
-                nxi = f[3];
-            }
+            const int li = (ci + 1) % kBufs, ri = (ci + 2) % kBufs;
+            const int hx = (ci + 3) % kBufs, nxi = (ci + 4) % kBufs;
             Key* cur_s = buf(ci);
             Key* L = buf(li);
             Key* R = buf(ri);
             const unsigned long long l = 2 * cur, r = 2 * cur + 1;
-            if (!pre) {
-                const unsigned long long tl0 = now();
-                acquire_children(cur, L, R);
-                pf_add(pfLvAcq, now() - tl0);
-            }
+            const unsigned long long tl0 = now();
+            acquire_children(cur, L, R);
+            if (cur == 1) pf_add(pfRsChild, now() - tl0);
+            else pf_add(pfLvAcq, now() - tl0);
             const unsigned long long tl2 = now();
-            pre = false;
             pf_add(pfLevels, 1);
             const uint32_t lk = sh->lk, rk = sh->rk;
             const bool lempty = !lk || L[0] == kMaxKey;
@@ -1021,7 +982,6 @@ struct HeapCta {
                 cta_store<Key, T>(node(cur), cur_s, K);
                 __syncthreads();
                 if (leader()) {
-                    if (extra) lane_unlock(extra, extra_rel);
                     if (lk) lane_unlock(l, sh->lrel);
                     if (rk) lane_unlock(r, sh->rrel);
                     lane_unlock(cur, cur_rel);
@@ -1077,11 +1037,9 @@ struct HeapCta {
             const uint32_t hi_rel = hi_left ? sh->lrel : sh->rrel;
             if (leader()) {
                 const uint32_t lo_rel = hi_left ? sh->rrel : sh->lrel;
-                if (extra) lane_unlock(extra, extra_rel);
                 if (lo_locked) lane_unlock(lo, lo_rel);
                 lane_unlock(cur, cur_rel);
             }
-            extra = 0;
             pf_add(pfLvMerge, tl3 - tl2);
             pf_add(pfLvRel, now() - tl3);
             if (cur == 1) pf_add(pfDelRootHold, now() - t_root);
