@@ -43,6 +43,19 @@ __device__ __forceinline__ bool state_cas(uint32_t* p, uint32_t expected, uint32
     return old == expected;
 }
 
+// Relaxed claim CAS: the data ordering comes from the acquire poll that saw
+// the holder's release, so the CAS only needs atomicity -- and, being
+// relaxed, it does not hold back the node loads issued right after it (an
+// acq_rel CAS would order them after its ~700-cycle round trip).
+__device__ __forceinline__ bool state_cas_relaxed(uint32_t* p, uint32_t expected, uint32_t desired) {
+    uint32_t old;
+    asm volatile("atom.relaxed.gpu.global.cas.b32 %0, [%1], %2, %3;"
+                 : "=r"(old)
+                 : "l"(p), "r"(expected), "r"(desired)
+                 : "memory");
+    return old == expected;
+}
+
 __device__ __forceinline__ void state_store_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

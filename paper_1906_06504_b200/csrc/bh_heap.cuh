@@ -41,6 +41,7 @@
 #pragma once
 
 #include "bh_device.cuh"
+#include "bh_select.cuh"
 
 namespace bh {
 
@@ -166,6 +167,12 @@ struct HeapCta {
         e.pad = 0;
         e.node = slot;
     }
+    __device__ void rec_for(unsigned long long op, uint16_t kind, unsigned long long slot) {
+        const unsigned long long saved = cur_op;
+        cur_op = op;
+        rec_lane(kind, slot);
+        cur_op = saved;
+    }
     __device__ __forceinline__ void rec(uint16_t kind, unsigned long long slot) {
         if (record && leader()) rec_lane(kind, slot);
     }
@@ -180,18 +187,89 @@ struct HeapCta {
     // of every CTA hammering one L2 word with CAS, and the hand-off costs one
     // store.  Mutual exclusion and FIFO hand-off order are the reference's
     // lock_avail(1)/unlock(1) semantics (heap.cpp:98-114).  Leader lane only.
-    __device__ void root_lock(bool record_it = true) {
+    // Queue slot line of ticket t: word 0 = hand-off flag (t<<1 granted,
+    // t<<1|1 served by a combiner), word 1 = request word (t<<1|1 when the
+    // waiter is a combinable insert), words 2-3 = its op index, words 4-9 =
+    // the combiner's response (rank, target slot, root sequence).
+    __device__ __forceinline__ uint32_t* qline(unsigned long long t) const {
+        return hv.root_flags + (t % kRootQueue) * kRootFlagStride;
+    }
+    // Returns true when a combiner ran this op's root phase instead of
+    // granting the lock (combinable = a BU full-batch insert, see
+    // serve_inserts).
+    __device__ bool root_lock(bool record_it = true, bool combinable = false) {
         const unsigned long long t = atomicAdd(&hdr->root_tail, 1ull);
-        uint32_t* f = hv.root_flags + (t % kRootQueue) * kRootFlagStride;
+        uint32_t* f = qline(t);
+        if (combinable) {
+            st_cg_u64(reinterpret_cast<unsigned long long*>(f + 2), cur_op);
+            state_store_release(f + 1, ((uint32_t)t << 1) | 1u);
+        }
+        const uint32_t granted = (uint32_t)t << 1;
         Backoff b;
-        while (state_load(f) != (uint32_t)t) b.pause();
+        uint32_t v;
+        while (((v = state_load(f)) & ~1u) != granted) b.pause();
         root_ticket = t;
+        if (v & 1u) return true;
         if (record_it) rec_lane(kEvAcq, 1);
+        return false;
     }
     __device__ void root_unlock(bool record_it = true) {
         if (record_it) rec_lane(kEvRel, 1);
         const unsigned long long nt = root_ticket + 1;
-        state_store_release(hv.root_flags + (nt % kRootQueue) * kRootFlagStride, (uint32_t)nt);
+        state_store_release(qline(nt), (uint32_t)nt << 1);
+    }
+
+    // Insert combining (flat combining inside the queue lock).  A BU full-
+    // batch insert holding the root, with the partial buffer empty, also runs
+    // the root phase of the queued waiters behind it that are BU full-batch
+    // inserts: each gets the next rank and its bit-reversed target slot,
+    // claimed INUSE under the root lock exactly as its own root phase would
+    // (heap.cpp:126-188, 295-308), in queue order -- so each op still
+    // linearizes at its rank assignment, one after the other, inside this
+    // root hold.  The waiter is woken with its response instead of the lock
+    // and goes straight to writing its target and climbing.  Warp 0, root
+    // held, own target claimed.  Returns the number of ops served.
+    __device__ uint32_t serve_inserts(unsigned long long nodes_after, unsigned long long seq_next) {
+        const uint32_t lane = threadIdx.x & 31u;
+        unsigned long long tail = 0;
+        if (lane == 0) tail = ld_cg_u64(&hdr->root_tail);
+        tail = __shfl_sync(0xFFFFFFFFu, tail, 0);
+        // root_ticket lives in the leader lane only
+        const unsigned long long mine = __shfl_sync(0xFFFFFFFFu, root_ticket, 0);
+        const unsigned long long t = mine + 1 + lane;
+        uint32_t* f = qline(t);
+        bool ok = t < tail && nodes_after + 1 + lane <= hv.max_nodes;
+        unsigned long long op = 0;
+        if (ok) {
+            ok = state_load(f + 1) == (((uint32_t)t << 1) | 1u);
+            if (ok) op = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 2));
+        }
+        const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
+        const uint32_t g = bad ? (uint32_t)__ffs(bad) - 1u : 32u;
+        unsigned long long target = 0;
+        if (lane < g) {
+            const unsigned long long rank = nodes_after + 1 + lane;
+            target = slot_for_rank(rank);
+            lane_claim(target, (1u << kAvail) | (1u << kDelMod));
+            st_cg_u64(reinterpret_cast<unsigned long long*>(f + 4), rank);
+            st_cg_u64(reinterpret_cast<unsigned long long*>(f + 6), target);
+            st_cg_u64(reinterpret_cast<unsigned long long*>(f + 8), seq_next + lane);
+        }
+        __syncwarp();
+        if (record) {  // each served op's root span, one after the other
+            for (uint32_t i = 0; i < g; ++i) {
+                const unsigned long long oi = __shfl_sync(0xFFFFFFFFu, op, i);
+                const unsigned long long ti = __shfl_sync(0xFFFFFFFFu, target, i);
+                if (lane == 0) {
+                    rec_for(oi, kEvAcq, 1);
+                    rec_for(oi, kEvAcq, ti);
+                    rec_for(oi, kEvRel, 1);
+                }
+                __syncwarp();
+            }
+        }
+        if (lane < g) state_store_release(f, ((uint32_t)t << 1) | 1u);
+        return g;
     }
 
     // Non-root claim: wait for one of `accept` (bitmask of states), CAS it to
@@ -318,8 +396,12 @@ struct HeapCta {
         if (leader()) {
             uint32_t gated = 0;
             Backoff gb;
+            const bool combinable =
+                hv.variant == BH_BU && n == (uint32_t)K && (hv.flags & kDbgNoCombine) == 0;
+            bool served = false;
             for (;;) {
-                root_lock(false);
+                served = root_lock(false, combinable);
+                if (served) break;
                 const unsigned long long nd = ld_cg_u64(&hdr->node_count);
                 const unsigned long long pl = ld_cg_u64(&hdr->partial_len);
                 const unsigned long long sq = ld_cg_u64(&hdr->root_seq);
@@ -339,8 +421,20 @@ struct HeapCta {
                 root_unlock(false);
                 gb.pause();
             }
-            rec(kEvAcq, 1);
-            sh->owned = gated;
+            if (served) {
+                // a combiner ran the root phase: rank, claimed target, sequence
+                const unsigned long long* f =
+                    reinterpret_cast<const unsigned long long*>(qline(root_ticket));
+                sh->nodes = ld_cg_u64(f + 2) - 1;  // words 4-5: rank
+                sh->plen = 0;
+                sh->seq = ld_cg_u64(f + 4);         // words 8-9
+                sh->owned = 1;                      // counted in the climbers gate
+                sh->act = 1;
+            } else {
+                rec(kEvAcq, 1);
+                sh->owned = gated;
+                sh->act = 0;
+            }
         }
         const unsigned long long t2 = now();
         __syncthreads();
@@ -348,6 +442,7 @@ struct HeapCta {
         const uint32_t plen = (uint32_t)sh->plen;
         const unsigned long long seq = sh->seq;
         const bool gated = sh->owned != 0;
+        const bool served = sh->act != 0;
         const bool full = n + plen >= (uint32_t)K;
         if (full && nodes == hv.max_nodes) {  // heap.cpp:129-135
             if (leader()) lane_unlock(1);
@@ -355,7 +450,7 @@ struct HeapCta {
             status(opi, BH_E_CAPACITY, 0, ~0ull);
             return;
         }
-        if (leader()) st_cg_u64(&hdr->root_seq, seq + 1);
+        if (leader() && !served) st_cg_u64(&hdr->root_seq, seq + 1);
         count(cInserts);
         pf_add(pfInsOps, 1);
         pf_add(pfInsSort, t1 - t0);
@@ -403,7 +498,7 @@ struct HeapCta {
         if (total > (uint32_t)K) cta_store<Key, T>(partial, comb + K, total - K);
         note_partial(total - K);
         const unsigned long long rank = nodes + 1;
-        if (leader()) {
+        if (leader() && !served) {
             if (plen || total != (uint32_t)K) st_cg_u64(&hdr->partial_len, total - K);
             st_cg_u64(&hdr->node_count, rank);
         }
@@ -421,7 +516,8 @@ struct HeapCta {
         if (hv.variant == BH_TD) {
             insert_td(target, comb, t2);
         } else {
-            insert_bu(target, comb, t2);
+            const bool can_serve = plen == 0 && n == (uint32_t)K && (hv.flags & kDbgNoCombine) == 0;
+            insert_bu(target, comb, t2, served, can_serve, rank, seq);
             if (gated && leader()) gate_leave(true);
         }
         status(opi, BH_OK, 0, seq);
@@ -545,11 +641,13 @@ struct HeapCta {
                 continue;
             }
             // kMerge: load the node while the leader's CAS claims it
-            cta_load<Key, T>(nd, node(next), K);
+            uint32_t ok = 0;
             if (leader()) {
                 const uint32_t w = sh->cw[0];
-                sh->ok[0] = state_cas(st(next), w, swith(w, kInUse));
+                ok = state_cas_relaxed(st(next), w, swith(w, kInUse));
             }
+            cta_load<Key, T>(nd, node(next), K);
+            if (leader()) sh->ok[0] = ok;
             __syncthreads();
             if (!sh->ok[0]) continue;  // lost the race: decide again
             if (leader()) rec(kEvAcq, next);
@@ -580,14 +678,36 @@ struct HeapCta {
     }
 
     // insert_bu (heap.cpp:295-373).  Root held on entry.
-    __device__ void insert_bu(unsigned long long target, Key* bat, unsigned long long t_root) {
+    // `served`: a combiner already claimed the target (serve_inserts);
+    // `can_serve`: this op may combine the waiters behind it.
+    __device__ void insert_bu(unsigned long long target, Key* bat, unsigned long long t_root, bool served,
+                              bool can_serve, unsigned long long rank, unsigned long long seq) {
         Key* par = bat == buf(4) ? buf(1) : buf(4);
         Key* cu = buf(5);
-        if (leader()) {
-            lane_claim(target, (1u << kAvail) | (1u << kDelMod));
-            rec(kEvAcq, target);
-            // The target is ours (INUSE): let the root go before writing it.
-            root_unlock();
+        if (!served) {
+            if (leader()) {
+                lane_claim(target, (1u << kAvail) | (1u << kDelMod));
+                rec(kEvAcq, target);
+            }
+            if (can_serve && threadIdx.x < 32) {
+                __syncwarp();
+                if (leader()) rec_lane(kEvRel, 1);  // this op's own root span ends here
+                const uint32_t g = serve_inserts(rank, seq + 1);
+                if (leader()) {
+                    if (g) {
+                        st_cg_u64(&hdr->node_count, rank + g);
+                        st_cg_u64(&hdr->root_seq, seq + 1 + g);
+                        atomicAdd(gate_mine(true), (unsigned long long)g);
+                        root_ticket += g;
+                        count(cCombined, g);
+                    }
+                    // The target is ours (INUSE): let the root go before writing it.
+                    root_unlock(false);
+                }
+            } else if (leader()) {
+                // The target is ours (INUSE): let the root go before writing it.
+                root_unlock();
+            }
         }
         pf_add(pfInsRootHold, now() - t_root);
         const unsigned long long t3 = now();
@@ -620,11 +740,13 @@ struct HeapCta {
                     }
                 }
                 __syncthreads();
-                cta_load<Key, T>(par, node(parent), K);
+                uint32_t ok = 1;
                 if (leader() && sh->ok[0] == 0) {
                     const uint32_t w = sh->cw[0];
-                    sh->ok[0] = state_cas(st(parent), w, swith(w, kInUse));
+                    ok = state_cas_relaxed(st(parent), w, swith(w, kInUse));
                 }
+                cta_load<Key, T>(par, node(parent), K);
+                if (leader() && sh->ok[0] == 0) sh->ok[0] = ok;
                 __syncthreads();
                 if (sh->ok[0]) break;
             }
@@ -663,11 +785,13 @@ struct HeapCta {
                 }
                 __syncthreads();
                 if (!sh->owned) break;
-                cta_load<Key, T>(cu, node(cur), K);
+                uint32_t ok = 0;
                 if (leader()) {
                     const uint32_t w = sh->cw[1];
-                    sh->ok[1] = state_cas(st(cur), w, swith(w, kInUse));
+                    ok = state_cas_relaxed(st(cur), w, swith(w, kInUse));
                 }
+                cta_load<Key, T>(cu, node(cur), K);
+                if (leader()) sh->ok[1] = ok;
                 __syncthreads();
                 if (sh->ok[1]) break;
             }
@@ -742,12 +866,19 @@ struct HeapCta {
             }
             __syncthreads();
             const uint32_t cl = ((pending & 1u) && sh->claim[0]) | (((pending & 2u) && sh->claim[1]) << 1);
+            // the claim CAS goes out first and relaxed, so the key loads below
+            // travel in the same round trip (the acquire was the poll)
+            uint32_t ok = 0;
+            if (threadIdx.x < 2 && ((cl >> threadIdx.x) & 1u)) {
+                const unsigned long long slot = 2 * cur + threadIdx.x;
+                const uint32_t w = sh->cw[threadIdx.x];
+                ok = state_cas_relaxed(st(slot), w, swith(w, kInUse));
+            }
             if (cl & 1u) cta_load<Key, T>(L, node(2 * cur), K);
             if (cl & 2u) cta_load<Key, T>(R, node(2 * cur + 1), K);
             if (threadIdx.x < 2 && ((cl >> threadIdx.x) & 1u)) {
                 const unsigned long long slot = 2 * cur + threadIdx.x;
                 const uint32_t w = sh->cw[threadIdx.x];
-                const uint32_t ok = state_cas(st(slot), w, swith(w, kInUse));
                 sh->ok[threadIdx.x] = ok;
                 if (ok) {
                     rec_lane(kEvAcq, slot);
@@ -902,14 +1033,17 @@ struct HeapCta {
             if (leader()) lane_poll_last(last);
             __syncthreads();
             const uint32_t act = sh->act;
+            uint32_t ok = 0;
+            if (act == kTake && leader()) {
+                const uint32_t w = sh->cw[2];
+                ok = state_cas_relaxed(st(last), w, swith(w, kInUse));
+            }
             cta_load<Key, T>(cur_s, node(act == kTake ? last : 1), K);
             if (act == kCoop) {
                 __syncthreads();
                 break;
             }
             if (leader()) {
-                const uint32_t w = sh->cw[2];
-                const uint32_t ok = state_cas(st(last), w, swith(w, kInUse));
                 sh->ok[2] = ok;
                 if (ok) rec_lane(kEvAcq, last);
             }
@@ -966,6 +1100,7 @@ struct HeapCta {
             const unsigned long long tl2 = now();
             pf_add(pfLevels, 1);
             const uint32_t lk = sh->lk, rk = sh->rk;
+            const uint32_t lrel = sh->lrel, rrel = sh->rrel;
             const bool lempty = !lk || L[0] == kMaxKey;
             const bool rempty = !rk || R[0] == kMaxKey;
             const Key cmax = cur_s[K - 1];
@@ -982,8 +1117,8 @@ struct HeapCta {
                 cta_store<Key, T>(node(cur), cur_s, K);
                 __syncthreads();
                 if (leader()) {
-                    if (lk) lane_unlock(l, sh->lrel);
-                    if (rk) lane_unlock(r, sh->rrel);
+                    if (lk) lane_unlock(l, lrel);
+                    if (rk) lane_unlock(r, rrel);
                     lane_unlock(cur, cur_rel);
                 }
                 if (cur == 1) pf_add(pfDelRootHold, now() - t_root);
@@ -1007,46 +1142,63 @@ struct HeapCta {
                 merge_children = true;
             }
             const unsigned long long hi = hi_left ? l : r;
+            const unsigned long long lo = hi_left ? r : l;
+            const uint32_t lo_locked = hi_left ? rk : lk;
+            const uint32_t hi_rel = hi_left ? lrel : rrel;
+            const uint32_t lo_rel = hi_left ? rrel : lrel;
             // warm L2 with the next level while this one merges
             prefetch_node(2 * hi);
             prefetch_node(2 * hi + 1);
+            // Only the first halves of the two merges decide the node's new
+            // batch (the k smallest of cur U L U R); the node is released as
+            // soon as it is written, and the second halves (the carried batch
+            // and the lo child's batch) are finished afterwards, on two
+            // thread groups side by side.
             Key* hdata = hi_left ? L : R;
             if (merge_children) {
-                Key* H = buf(hx);
-                cta_merge_full<Key, K, T>(L, R, H, node(hi_left ? r : l));
+                cta_merge_half<Key, K, T, false, false>(L, R, buf(hx), threadIdx.x);
                 count(cMerges);
                 __syncthreads();
-                hdata = H;
+                hdata = buf(hx);
             }
-            const unsigned long long lo = hi_left ? r : l;
-            const uint32_t lo_locked = hi_left ? rk : lk;
+            const bool merge_cur = !(elide && !needs_merge_full<Key, K>(cur_s, hdata));
             int next_ci;
-            if (elide && !needs_merge_full<Key, K>(cur_s, hdata)) {
+            if (!merge_cur) {
                 // early stop ruled out the ordered case: a full inversion
                 count(cElided);
                 cta_store<Key, T>(node(cur), hdata, K);
                 next_ci = ci;  // old cur batch moves down into hi
             } else {
-                cta_merge_full<Key, K, T>(cur_s, hdata, node(cur), buf(nxi));
+                cta_merge_half<Key, K, T, false, true>(cur_s, hdata, node(cur), threadIdx.x);
                 count(cMerges);
                 next_ci = nxi;
             }
             count(cVisits);
             const unsigned long long tl3 = now();
             __syncthreads();
-            const uint32_t hi_rel = hi_left ? sh->lrel : sh->rrel;
             if (leader()) {
-                const uint32_t lo_rel = hi_left ? sh->rrel : sh->lrel;
-                if (lo_locked) lane_unlock(lo, lo_rel);
                 lane_unlock(cur, cur_rel);
+                if (lo_locked && !merge_children) lane_unlock(lo, lo_rel);  // unchanged
             }
+            if (cur == 1) pf_add(pfDelRootHold, now() - t_root);
+            using HS = HalfShape<K, T>;
+            if constexpr (HS::kPair) {
+                if (threadIdx.x < (uint32_t)HS::kThreads) {
+                    if (merge_cur) cta_merge_half<Key, K, T, true, false>(cur_s, hdata, buf(nxi), threadIdx.x);
+                } else if (merge_children) {
+                    cta_merge_half<Key, K, T, true, true>(L, R, node(lo), threadIdx.x - HS::kThreads);
+                }
+            } else {
+                if (merge_cur) cta_merge_half<Key, K, T, true, false>(cur_s, hdata, buf(nxi), threadIdx.x);
+                if (merge_children) cta_merge_half<Key, K, T, true, true>(L, R, node(lo), threadIdx.x);
+            }
+            __syncthreads();
+            if (leader() && lo_locked && merge_children) lane_unlock(lo, lo_rel);
             pf_add(pfLvMerge, tl3 - tl2);
             pf_add(pfLvRel, now() - tl3);
-            if (cur == 1) pf_add(pfDelRootHold, now() - t_root);
             cur = hi;
             cur_rel = hi_rel;
             ci = next_ci;
-            __syncthreads();  // sh->lk/rk/lrel/rrel are rewritten next level
         }
     }
 };

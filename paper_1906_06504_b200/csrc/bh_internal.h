@@ -28,6 +28,7 @@ constexpr uint32_t kRootFlagStride = 32;  // uint32 words
 constexpr uint32_t kDbgSeqRefill = 0x100;       // reference refill order in every delete
 constexpr uint32_t kDbgWriteUnderRoot = 0x200;  // BU target written before the root release
 constexpr uint32_t kDbgSerialLanes = 0x400;     // claim children one after the other
+constexpr uint32_t kDbgNoCombine = 0x800;       // no insert combining in the root queue lock
 
 // Heap header, root-lock guarded (reference heap.hpp:173-177).  One cache
 // line; the partial buffer follows in its own allocation.
@@ -57,6 +58,7 @@ enum CounterIdx {
     cVisits,
     cCoop,
     cMaxPartial,
+    cCombined,  // inserts whose root phase a combiner ran (not a reference counter)
     kNumCounters
 };
 
