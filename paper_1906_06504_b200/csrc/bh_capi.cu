@@ -385,8 +385,8 @@ int bh_create(bh_heap** out, int variant, uint32_t k, uint32_t max_nodes, uint32
     cudaMemsetAsync(h->d_root_flags, 0xFF, (size_t)kRootQueue * kRootFlagStride * 4, h->stream);
     cudaMemsetAsync(h->d_root_flags, 0, 4, h->stream);
     if (flags & BH_FLAG_PROFILE) {
-        if ((e = cudaMalloc(&h->d_prof, 32 * 8)) != cudaSuccess) return cleanup(cuda_fail(e, "prof"));
-        cudaMemsetAsync(h->d_prof, 0, 32 * 8, h->stream);
+        if ((e = cudaMalloc(&h->d_prof, kProfWords * 8)) != cudaSuccess) return cleanup(cuda_fail(e, "prof"));
+        cudaMemsetAsync(h->d_prof, 0, kProfWords * 8, h->stream);
     }
     if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) return cleanup(cuda_fail(e, "init"));
     int rc = key_bits == 32 ? info_u32(k, &h->kinfo) : info_u64(k, &h->kinfo);
@@ -748,14 +748,26 @@ int bh_profile(bh_heap* h, uint64_t* out, uint32_t cap, int reset) {
     if (!h || !out) return fail(BH_E_CONFIG, "null argument");
     if (!h->d_prof) return fail(BH_E_CONFIG, "heap was not created with BH_FLAG_PROFILE");
     BH_CUDA(cudaSetDevice(h->device));
-    uint64_t buf[32];
-    BH_CUDA(cudaMemcpyAsync(buf, h->d_prof, sizeof(buf), cudaMemcpyDeviceToHost, h->aux));
+    const uint32_t n = std::min<uint32_t>(cap, kProfWords);
+    // aux is a non-blocking stream: this copy also works while a run is in
+    // flight (debug builds read their per-CTA wait notes this way)
+    BH_CUDA(cudaMemcpyAsync(out, h->d_prof, n * 8, cudaMemcpyDeviceToHost, h->aux));
     BH_CUDA(cudaStreamSynchronize(h->aux));
-    std::memcpy(out, buf, std::min<uint32_t>(cap, 32) * 8);
     if (reset) {
-        BH_CUDA(cudaMemsetAsync(h->d_prof, 0, sizeof(buf), h->aux));
+        BH_CUDA(cudaMemsetAsync(h->d_prof, 0, kProfWords * 8, h->aux));
         BH_CUDA(cudaStreamSynchronize(h->aux));
     }
+    return BH_OK;
+}
+
+// Debug: the raw state array (kStateStride words per slot), copied on the
+// non-blocking aux stream so it can be read while a run is stuck.
+extern "C" __attribute__((visibility("default"))) int bh_debug_states(bh_heap* h, uint32_t* out, uint64_t words) {
+    if (!h || !out) return fail(BH_E_CONFIG, "null argument");
+    BH_CUDA(cudaSetDevice(h->device));
+    const uint64_t n = std::min<uint64_t>(words, (h->slot_count + 1) * kStateStride);
+    BH_CUDA(cudaMemcpyAsync(out, h->d_states, n * 4, cudaMemcpyDeviceToHost, h->aux));
+    BH_CUDA(cudaStreamSynchronize(h->aux));
     return BH_OK;
 }
 

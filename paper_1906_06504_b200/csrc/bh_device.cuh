@@ -88,6 +88,56 @@ __device__ __forceinline__ void cta_prefetch_l2(const void* p, uint32_t bytes, u
     }
 }
 
+// Barrier of a thread group: id 0 is the whole CTA, ids 1..15 are named
+// barriers over `nthr` threads (a multiple of 32).  Lets two halves of a CTA
+// run independent protocol steps side by side.
+__device__ __forceinline__ void grp_sync(uint32_t id, uint32_t nthr) {
+    if (id == 0)
+        __syncthreads();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory");
+}
+
+// Group versions of the node moves (thread `tid` of `nthr`).
+template <typename Key>
+__device__ __forceinline__ void grp_load(Key* __restrict__ s, const Key* __restrict__ g, uint32_t n, uint32_t tid,
+                                         uint32_t nthr) {
+    const uint32_t bytes = n * (uint32_t)sizeof(Key);
+    if (((bytes | (uint32_t)(uintptr_t)g) & 15u) == 0) {
+        const uint4* gv = reinterpret_cast<const uint4*>(g);
+        uint4* sv = reinterpret_cast<uint4*>(s);
+        for (uint32_t i = tid; i < bytes / 16; i += nthr) sv[i] = __ldcg(gv + i);
+    } else {
+        for (uint32_t i = tid; i < n; i += nthr) s[i] = __ldcg(g + i);
+    }
+}
+
+template <typename Key>
+__device__ __forceinline__ void grp_store(Key* __restrict__ g, const Key* __restrict__ s, uint32_t n, uint32_t tid,
+                                          uint32_t nthr) {
+    const uint32_t bytes = n * (uint32_t)sizeof(Key);
+    if (((bytes | (uint32_t)(uintptr_t)g) & 15u) == 0) {
+        uint4* gv = reinterpret_cast<uint4*>(g);
+        const uint4* sv = reinterpret_cast<const uint4*>(s);
+        for (uint32_t i = tid; i < bytes / 16; i += nthr) __stcg(gv + i, sv[i]);
+    } else {
+        for (uint32_t i = tid; i < n; i += nthr) __stcg(g + i, s[i]);
+    }
+}
+
+template <typename Key>
+__device__ __forceinline__ void grp_fill_max(Key* g, uint32_t n, uint32_t tid, uint32_t nthr) {
+    const uint32_t bytes = n * (uint32_t)sizeof(Key);
+    if (((bytes | (uint32_t)(uintptr_t)g) & 15u) == 0) {
+        uint4 fill;
+        fill.x = fill.y = fill.z = fill.w = 0xFFFFFFFFu;
+        uint4* gv = reinterpret_cast<uint4*>(g);
+        for (uint32_t i = tid; i < bytes / 16; i += nthr) __stcg(gv + i, fill);
+    } else {
+        for (uint32_t i = tid; i < n; i += nthr) __stcg(g + i, ~Key(0));
+    }
+}
+
 // Spin backoff (reference Backoff, proj/src/heap.cpp:18-31: 2^0..2^5 pause
 // rounds, then yield).  On the GPU a waiting CTA sleeps in growing steps so the
 // lock holder's SM and the contended L2 slice stay free.

@@ -84,16 +84,36 @@ enum ProfIdx {
     pfLvLoad,   //   (unused: loads overlap the claims)
     pfLvMerge,  //   both merges
     pfLvRel,    //   write-back barrier + releases
+    pfServed,   // inserts served by a combiner
+    pfServeHolds,  // root holds that served >= 1 waiter
+    pfBuParent, // BU climb: park -> parent claimed (cycles)
+    pfBuRetake, // BU climb: re-take of the parked slot (cycles)
+    pfBuLevels, // BU climb levels
     kNumProf
 };
+
+// Debug builds (-DBH_DEBUG_WAIT) record, per CTA, the source line of the
+// spin loop it is in and how many pauses it has made, in the profile buffer
+// (words kDbgWaitBase + 4*cta ...), readable while the kernel runs.
+#ifdef BH_DEBUG_WAIT
+#define BH_WAIT_NOTE(line) wait_note(line)
+#define BH_WAIT_NOTE2(slot, w) wait_note2(slot, w)
+#define BH_OWN(slot) dbg_own(slot, __LINE__)
+#else
+#define BH_OWN(slot) ((void)0)
+#define BH_WAIT_NOTE(line) ((void)0)
+#define BH_WAIT_NOTE2(slot, w) ((void)0)
+#endif
+constexpr uint32_t kDbgWaitBase = 32;
 
 template <typename Key, int K, int T>
 struct HeapCta {
     static constexpr Key kMaxKey = KeyLimits<Key>::kMax;
-    static constexpr int kBufs = 6;
+    static constexpr int kBufs = 8;
     static constexpr uint32_t kNodeBytes = K * sizeof(Key);
     // prefetches are issued by warps other than the leader's
     static constexpr uint32_t kPfFirst = T > 64 ? 64 : 0;
+    static constexpr uint32_t kRefillAhead = T > 64 ? 8 : 0;
 
     HeapView hv;
     RunView rv;
@@ -129,6 +149,23 @@ struct HeapCta {
         prof = h.prof != nullptr;
     }
 
+    __device__ void wait_note(int line) {
+        if (!hv.prof) return;
+        volatile unsigned long long* d = hv.prof + kDbgWaitBase + 4ull * blockIdx.x;
+        d[0] = (unsigned long long)line | ((unsigned long long)threadIdx.x << 32);
+        d[1] = d[1] + 1;
+        d[2] = cur_op;
+    }
+    __device__ void dbg_own(unsigned long long slot, int line) {
+        volatile uint32_t* o = states + slot * kStateStride;
+        o[1] = (blockIdx.x + 1u) | ((uint32_t)line << 16);
+        o[2] = (uint32_t)cur_op;
+    }
+    __device__ void wait_note2(unsigned long long slot, uint32_t w) {
+        if (!hv.prof) return;
+        volatile unsigned long long* d = hv.prof + kDbgWaitBase + 4ull * blockIdx.x;
+        d[3] = (slot << 32) | w;
+    }
     __device__ __forceinline__ Key* buf(int i) const { return bufs + i * K; }
     __device__ __forceinline__ bool leader() const { return threadIdx.x == 0; }
     __device__ __forceinline__ Key* node(unsigned long long slot) const { return keys + (slot - 1) * K; }
@@ -207,7 +244,7 @@ struct HeapCta {
         const uint32_t granted = (uint32_t)t << 1;
         Backoff b;
         uint32_t v;
-        while (((v = state_load(f)) & ~1u) != granted) b.pause();
+        while (((v = state_load(f)) & ~1u) != granted) { b.pause(); BH_WAIT_NOTE(__LINE__); }
         root_ticket = t;
         if (v & 1u) return true;
         if (record_it) rec_lane(kEvAcq, 1);
@@ -279,8 +316,11 @@ struct HeapCta {
         Backoff b;
         for (;;) {
             const uint32_t w = state_load(p);
-            if (((accept >> sget(w)) & 1u) && state_cas(p, w, swith(w, kInUse))) return sget(w);
-            b.pause();
+            if (((accept >> sget(w)) & 1u) && state_cas(p, w, swith(w, kInUse))) {
+                BH_OWN(slot);
+                return sget(w);
+            }
+            { b.pause(); BH_WAIT_NOTE(__LINE__); }
         }
     }
     // unlock (heap.cpp:111-114) of a node this lane's CTA holds INUSE.  The
@@ -291,6 +331,9 @@ struct HeapCta {
             return;
         }
         rec_lane(kEvRel, slot);
+#ifdef BH_DEBUG_WAIT
+        { volatile uint32_t* o = states + slot * kStateStride; o[1] = 0xDEAD0000u | (uint32_t)(blockIdx.x & 0xFFFF); }
+#endif
         state_release(st(slot), kInUse, release_as);
     }
 
@@ -419,7 +462,7 @@ struct HeapCta {
                     break;
                 }
                 root_unlock(false);
-                gb.pause();
+                { gb.pause(); BH_WAIT_NOTE(__LINE__); }
             }
             if (served) {
                 // a combiner ran the root phase: rank, claimed target, sequence
@@ -560,7 +603,7 @@ struct HeapCta {
                 const uint32_t s = sget(w);
                 // (DELMOD: BU heaps only; never seen in TD heaps)
                 if ((s == kAvail || s == kDelMod) && state_cas(p, w, swith(w, kTarget))) break;
-                b.pause();
+                { b.pause(); BH_WAIT_NOTE(__LINE__); }
             }
         }
         cta_load<Key, T>(nd, node(1), K);  // root keys, in the claim's round trip
@@ -589,7 +632,7 @@ struct HeapCta {
                             act = kShip;
                             break;
                         } else {
-                            b.pause();
+                            { b.pause(); BH_WAIT_NOTE(__LINE__); }
                         }
                     }
                 } else {
@@ -605,7 +648,7 @@ struct HeapCta {
                             act = kSkip;  // frozen empty while we hold its ancestor
                             break;
                         } else {
-                            b.pause();
+                            { b.pause(); BH_WAIT_NOTE(__LINE__); }
                         }
                     }
                 }
@@ -672,7 +715,7 @@ struct HeapCta {
             } else if (s != kInUse) {
                 return;  // AVAIL, or a later insert owns the slot now
             } else {
-                b.pause();
+                { b.pause(); BH_WAIT_NOTE(__LINE__); }
             }
         }
     }
@@ -700,6 +743,8 @@ struct HeapCta {
                         atomicAdd(gate_mine(true), (unsigned long long)g);
                         root_ticket += g;
                         count(cCombined, g);
+                        pf_add(pfServed, g);
+                        pf_add(pfServeHolds, 1);
                     }
                     // The target is ours (INUSE): let the root go before writing it.
                     root_unlock(false);
@@ -719,6 +764,8 @@ struct HeapCta {
         unsigned long long cur = target;  // held
         while (cur != 1) {
             const unsigned long long parent = cur >> 1;
+            const unsigned long long tc0 = now();
+            pf_add(pfBuLevels, 1);
             // ---- park, then claim the parent with its keys in flight ----
             if (leader()) lane_unlock(cur, kInsHold);
             for (;;) {
@@ -733,7 +780,7 @@ struct HeapCta {
                         for (;;) {
                             w = state_load(pp);
                             if (sget(w) == kAvail || sget(w) == kDelMod) break;
-                            b.pause();
+                            { b.pause(); BH_WAIT_NOTE(__LINE__); }
                         }
                         sh->cw[0] = w;
                         sh->ok[0] = 0;
@@ -751,6 +798,8 @@ struct HeapCta {
                 if (sh->ok[0]) break;
             }
             if (parent != 1 && leader()) rec(kEvAcq, parent);
+            const unsigned long long tc1 = now();
+            pf_add(pfBuParent, tc1 - tc0);
             if (par[0] == kMaxKey) {
                 // parent was deleted: the subtree with our parked slot is gone
                 if (leader()) {
@@ -778,7 +827,7 @@ struct HeapCta {
                         } else if (s != kInUse) {
                             break;  // AVAIL (or re-claimed): consumed
                         } else {
-                            b.pause();  // INUSE: a deleter is working on it
+                            { b.pause(); BH_WAIT_NOTE(__LINE__); }  // INUSE: a deleter is working on it
                         }
                     }
                     sh->owned = owned;
@@ -795,6 +844,7 @@ struct HeapCta {
                 __syncthreads();
                 if (sh->ok[1]) break;
             }
+            pf_add(pfBuRetake, now() - tc1);
             if (sh->owned) {
                 if (leader()) rec(kEvAcq, cur);
                 if (cu[0] >= par[K - 1]) {
@@ -831,10 +881,14 @@ struct HeapCta {
     // the claiming CAS.  TARGET/MARKED children are frozen empty (skipped);
     // INSHOLD children are taken over and released as DELMOD.  Sets
     // sh->lk/rk and sh->lrel/rrel.  Ends with a barrier.
-    __device__ void acquire_children(unsigned long long cur, Key* L, Key* R) {
+    // The calling thread group is threads [base, base + nthr) with barrier id
+    // `bar` (0 = the whole CTA, nthr = T).
+    __device__ void acquire_children(unsigned long long cur, Key* L, Key* R, uint32_t base = 0,
+                                     uint32_t nthr = T, uint32_t bar = 0) {
+        const uint32_t gt = threadIdx.x - base;
         uint32_t pending = 3u;
-        if (threadIdx.x < 2) {
-            if (threadIdx.x == 0) {
+        if (gt < 2) {
+            if (gt == 0) {
                 sh->lk = 0;
                 sh->lrel = kAvail;
             } else {
@@ -844,8 +898,8 @@ struct HeapCta {
         }
         const unsigned long long t = now();
         for (;;) {
-            if (threadIdx.x < 2 && ((pending >> threadIdx.x) & 1u)) {
-                const unsigned long long slot = 2 * cur + threadIdx.x;
+            if (gt < 2 && ((pending >> gt) & 1u)) {
+                const unsigned long long slot = 2 * cur + gt;
                 uint32_t claim = 0, w = 0;
                 if (slot <= hv.slot_count) {
                     uint32_t* p = st(slot);
@@ -858,32 +912,33 @@ struct HeapCta {
                             break;
                         }
                         if (s == kTarget || s == kMarked) break;  // frozen empty
-                        b.pause();
+                        { b.pause(); BH_WAIT_NOTE(__LINE__); BH_WAIT_NOTE2(slot, w); }
                     }
                 }
-                sh->claim[threadIdx.x] = claim;
-                sh->cw[threadIdx.x] = w;
+                sh->claim[gt] = claim;
+                sh->cw[gt] = w;
             }
-            __syncthreads();
+            grp_sync(bar, nthr);
             const uint32_t cl = ((pending & 1u) && sh->claim[0]) | (((pending & 2u) && sh->claim[1]) << 1);
             // the claim CAS goes out first and relaxed, so the key loads below
             // travel in the same round trip (the acquire was the poll)
             uint32_t ok = 0;
-            if (threadIdx.x < 2 && ((cl >> threadIdx.x) & 1u)) {
-                const unsigned long long slot = 2 * cur + threadIdx.x;
-                const uint32_t w = sh->cw[threadIdx.x];
+            if (gt < 2 && ((cl >> gt) & 1u)) {
+                const unsigned long long slot = 2 * cur + gt;
+                const uint32_t w = sh->cw[gt];
                 ok = state_cas_relaxed(st(slot), w, swith(w, kInUse));
+                if (ok) BH_OWN(slot);
             }
-            if (cl & 1u) cta_load<Key, T>(L, node(2 * cur), K);
-            if (cl & 2u) cta_load<Key, T>(R, node(2 * cur + 1), K);
-            if (threadIdx.x < 2 && ((cl >> threadIdx.x) & 1u)) {
-                const unsigned long long slot = 2 * cur + threadIdx.x;
-                const uint32_t w = sh->cw[threadIdx.x];
-                sh->ok[threadIdx.x] = ok;
+            if (cl & 1u) grp_load<Key>(L, node(2 * cur), K, gt, nthr);
+            if (cl & 2u) grp_load<Key>(R, node(2 * cur + 1), K, gt, nthr);
+            if (gt < 2 && ((cl >> gt) & 1u)) {
+                const unsigned long long slot = 2 * cur + gt;
+                const uint32_t w = sh->cw[gt];
+                sh->ok[gt] = ok;
                 if (ok) {
                     rec_lane(kEvAcq, slot);
                     const uint32_t rel = sget(w) == kInsHold ? kDelMod : kAvail;
-                    if (threadIdx.x == 0) {
+                    if (gt == 0) {
                         sh->lk = 1;
                         sh->lrel = rel;
                     } else {
@@ -892,7 +947,7 @@ struct HeapCta {
                     }
                 }
             }
-            __syncthreads();
+            grp_sync(bar, nthr);
             uint32_t still = 0;
             if ((cl & 1u) && !sh->ok[0]) still |= 1u;
             if ((cl & 2u) && !sh->ok[1]) still |= 2u;
@@ -923,11 +978,44 @@ struct HeapCta {
             }
             if (s == kTarget && state_cas(p, w, swith(w, kMarked))) {
                 Backoff wb;
-                while (sget(state_load(p)) != kAvail) wb.pause();
+                while (sget(state_load(p)) != kAvail) { wb.pause(); BH_WAIT_NOTE(__LINE__); }
                 sh->act = kCoop;
                 return;
             }
-            b.pause();
+            { b.pause(); BH_WAIT_NOTE(__LINE__); }
+        }
+    }
+
+    // refill_root_from(last), claim + copy + blank + release, by threads
+    // [base, base + nthr) with barrier `bar`.  The refill batch lands in dst.
+    __device__ void refill_last(unsigned long long last, Key* dst, uint32_t base, uint32_t nthr, uint32_t bar) {
+        const uint32_t gt = threadIdx.x - base;
+        for (;;) {
+            if (gt == 0) lane_poll_last(last);
+            grp_sync(bar, nthr);
+            const uint32_t act = sh->act;
+            uint32_t ok = 0;
+            if (act == kTake && gt == 0) {
+                const uint32_t w = sh->cw[2];
+                ok = state_cas_relaxed(st(last), w, swith(w, kInUse));
+                if (ok) BH_OWN(last);
+            }
+            grp_load<Key>(dst, node(act == kTake ? last : 1), K, gt, nthr);
+            if (act == kCoop) {
+                grp_sync(bar, nthr);
+                return;
+            }
+            if (gt == 0) {
+                sh->ok[2] = ok;
+                if (ok) rec_lane(kEvAcq, last);
+            }
+            grp_sync(bar, nthr);
+            if (sh->ok[2]) {
+                grp_fill_max<Key>(node(last), K, gt, nthr);
+                grp_sync(bar, nthr);
+                if (gt == 0) lane_unlock(last, sh->lastrel);
+                return;
+            }
         }
     }
 
@@ -951,7 +1039,7 @@ struct HeapCta {
                         break;
                     }
                     root_unlock(false);
-                    gb.pause();
+                    { gb.pause(); BH_WAIT_NOTE(__LINE__); }
                 }
                 rec(kEvAcq, 1);
             } else {
@@ -975,6 +1063,14 @@ struct HeapCta {
         const uint32_t plen = (uint32_t)sh->plen;
         const unsigned long long seq = sh->seq;
         Key* out = static_cast<Key*>(rv.out_pool) + o.offset;
+        // warm L2 with the refill nodes of the next few deletes (HBM-cold
+        // bottom-level nodes; the claim then hits L2)
+        if (threadIdx.x >= 32 && threadIdx.x < 32 + kRefillAhead && nodes > threadIdx.x - 32 + 5) {
+            const unsigned long long slot = slot_for_rank(nodes - 1 - (threadIdx.x - 32));
+            const char* a = reinterpret_cast<const char*>(node(slot));
+            for (uint32_t off = 0; off < kNodeBytes; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(st(slot)));
+        }
         pf_add(pfDelOps, 1);
         pf_add(pfDelRootWait, t1 - t0);
 
@@ -1020,40 +1116,29 @@ struct HeapCta {
             return;
         }
 
-        // ---- refill_root_from(last) (heap.cpp:467-531) in the reference's
-        // order: only the root is held while the last node is claimed, so the
-        // refill overlaps the wait for the predecessor still working on
-        // level 1, and its keys load in the same round trip as the claim ----
+        // ---- refill_root_from(last) (heap.cpp:467-531): only the root is
+        // held while the last node is claimed.  With nodes >= 4 the last node
+        // is below level 1, so one half of the CTA claims, copies, blanks and
+        // releases it while the other half claims the root's children (the
+        // first heapify level) -- the refill never waits on a child, so the
+        // reference's deadlock argument (last released before any child is
+        // awaited) still holds for the refill half, and the children half
+        // holds nothing but the root while it waits ----
         const unsigned long long last = slot_for_rank(nodes);
         Key* sp = buf(3);
         const unsigned long long ta = now();
         pf_add(pfRsHead, ta - t1);
         if (plen) cta_load<Key, T>(sp, partial, plen);
-        for (;;) {
-            if (leader()) lane_poll_last(last);
+        const bool split = T >= 64 && nodes >= 4;
+        if (split) {
+            constexpr uint32_t kHalf = T / 2;
+            if (threadIdx.x < kHalf)
+                refill_last(last, cur_s, 0, kHalf, 1);
+            else
+                acquire_children(1, buf(1), buf(2), kHalf, kHalf, 2);
             __syncthreads();
-            const uint32_t act = sh->act;
-            uint32_t ok = 0;
-            if (act == kTake && leader()) {
-                const uint32_t w = sh->cw[2];
-                ok = state_cas_relaxed(st(last), w, swith(w, kInUse));
-            }
-            cta_load<Key, T>(cur_s, node(act == kTake ? last : 1), K);
-            if (act == kCoop) {
-                __syncthreads();
-                break;
-            }
-            if (leader()) {
-                sh->ok[2] = ok;
-                if (ok) rec_lane(kEvAcq, last);
-            }
-            __syncthreads();
-            if (sh->ok[2]) {
-                cta_fill<Key, T>(node(last), kMaxKey, K);
-                __syncthreads();
-                if (leader()) lane_unlock(last, sh->lastrel);
-                break;
-            }
+        } else {
+            refill_last(last, cur_s, 0, T, 0);
         }
         const unsigned long long td = now();
         pf_add(pfRsLast, td - ta);
@@ -1073,7 +1158,7 @@ struct HeapCta {
             __syncthreads();
         }
         pf_add(pfRsFill, now() - td);
-        heapify_down(ci, t1);
+        heapify_down(ci, t1, split);
         if (gated && leader()) gate_leave(false);
         status(opi, BH_OK, K, seq);
         rec(kEvRes, 0);
@@ -1081,24 +1166,49 @@ struct HeapCta {
 
     // heapify_down (heap.cpp:591-667) with the carried batch in buf(ci).
     // Root held on entry.  Releases every lock it holds.
-    __device__ void heapify_down(int ci, unsigned long long t_root) {
+    //
+    // Per level (acquire_child, early stop, hi/lo with the tie fix, then the
+    // two merges of heap.cpp:637-660), scheduled for a short critical path:
+    //   phase 1  the node's new batch = first half of merge(cur, H), where H
+    //            is the first half of merge(L, R) (the k smallest of the
+    //            children); written, and the node released at once;
+    //   phase 2  threads [0, T/2) compute the carried batch (second half of
+    //            merge(cur, H)) and the lo child's batch (second half of
+    //            merge(L, R)) and release the lo child; threads [T/2, T)
+    //            meanwhile claim and load hi's children and, when they
+    //            interleave, already compute the next level's H.
+    // A node is held only for phase 1 of its own level; the next level's
+    // claim round trip and H merge run in the shadow of the second halves.
+    // Lock order, states and released contents are the reference's.
+    // `pre`: the root's children are already claimed, in buf(1) and buf(2).
+    __device__ void heapify_down(int ci, unsigned long long t_root, bool pre) {
+        constexpr bool kSplit = T >= 64;
+        constexpr uint32_t kHalf = kSplit ? T / 2 : T;
         unsigned long long cur = 1;
         uint32_t cur_rel = kAvail;
         const unsigned long long t_start = now();
+        auto free_buf = [](uint32_t used) { return __ffs(~used) - 1; };
+        int li, ri;
+        if (pre) {
+            li = 1;
+            ri = 2;
+        } else {
+            li = free_buf(1u << ci);
+            ri = free_buf((1u << ci) | (1u << li));
+        }
+        bool have = pre;  // children of cur claimed and loaded
+        int hx = -1;      // buffer holding H, when precomputed
         for (;;) {
-            // buffer plan: L, R, H, NX distinct from the carried batch
-            const int li = (ci + 1) % kBufs, ri = (ci + 2) % kBufs;
-            const int hx = (ci + 3) % kBufs, nxi = (ci + 4) % kBufs;
             Key* cur_s = buf(ci);
-            Key* L = buf(li);
-            Key* R = buf(ri);
             const unsigned long long l = 2 * cur, r = 2 * cur + 1;
             const unsigned long long tl0 = now();
-            acquire_children(cur, L, R);
+            if (!have) acquire_children(cur, buf(li), buf(ri));
             if (cur == 1) pf_add(pfRsChild, now() - tl0);
             else pf_add(pfLvAcq, now() - tl0);
             const unsigned long long tl2 = now();
             pf_add(pfLevels, 1);
+            Key* L = buf(li);
+            Key* R = buf(ri);
             const uint32_t lk = sh->lk, rk = sh->rk;
             const uint32_t lrel = sh->lrel, rrel = sh->rrel;
             const bool lempty = !lk || L[0] == kMaxKey;
@@ -1140,40 +1250,32 @@ struct HeapCta {
             } else {
                 hi_left = !(L[K - 1] > R[K - 1]);
                 merge_children = true;
+                count(cMerges);
             }
             const unsigned long long hi = hi_left ? l : r;
             const unsigned long long lo = hi_left ? r : l;
             const uint32_t lo_locked = hi_left ? rk : lk;
             const uint32_t hi_rel = hi_left ? lrel : rrel;
             const uint32_t lo_rel = hi_left ? rrel : lrel;
-            // warm L2 with the next level while this one merges
-            prefetch_node(2 * hi);
+            prefetch_node(2 * hi);  // warm L2 with the next level
             prefetch_node(2 * hi + 1);
-            // Only the first halves of the two merges decide the node's new
-            // batch (the k smallest of cur U L U R); the node is released as
-            // soon as it is written, and the second halves (the carried batch
-            // and the lo child's batch) are finished afterwards, on two
-            // thread groups side by side.
-            Key* hdata = hi_left ? L : R;
-            if (merge_children) {
-                cta_merge_half<Key, K, T, false, false>(L, R, buf(hx), threadIdx.x);
-                count(cMerges);
+            // ---- phase 1 ----
+            if (merge_children && hx < 0) {  // H not precomputed (root level)
+                hx = free_buf((1u << ci) | (1u << li) | (1u << ri));
+                cta_merge_half<Key, K, T, false, false>(L, R, buf(hx), threadIdx.x, T);
+                // every thread reads H's ends below (merge_cur decides the
+                // buffer plan), so the whole CTA waits for it
                 __syncthreads();
-                hdata = buf(hx);
             }
+            Key* hdata = merge_children ? buf(hx) : (hi_left ? L : R);
             const bool merge_cur = !(elide && !needs_merge_full<Key, K>(cur_s, hdata));
-            int next_ci;
-            if (!merge_cur) {
-                // early stop ruled out the ordered case: a full inversion
-                count(cElided);
-                cta_store<Key, T>(node(cur), hdata, K);
-                next_ci = ci;  // old cur batch moves down into hi
-            } else {
-                cta_merge_half<Key, K, T, false, true>(cur_s, hdata, node(cur), threadIdx.x);
-                count(cMerges);
-                next_ci = nxi;
-            }
+            if (merge_cur) count(cMerges);
+            else count(cElided);
             count(cVisits);
+            if (!merge_cur)  // early stop ruled out the ordered case: a full inversion
+                cta_store<Key, T>(node(cur), hdata, K);
+            else
+                cta_merge_half<Key, K, T, false, true>(cur_s, hdata, node(cur), threadIdx.x, T);
             const unsigned long long tl3 = now();
             __syncthreads();
             if (leader()) {
@@ -1181,30 +1283,63 @@ struct HeapCta {
                 if (lo_locked && !merge_children) lane_unlock(lo, lo_rel);  // unchanged
             }
             if (cur == 1) pf_add(pfDelRootHold, now() - t_root);
-            using HS = HalfShape<K, T>;
-            if constexpr (HS::kPair) {
-                if (threadIdx.x < (uint32_t)HS::kThreads) {
-                    if (merge_cur) cta_merge_half<Key, K, T, true, false>(cur_s, hdata, buf(nxi), threadIdx.x);
-                } else if (merge_children) {
-                    cta_merge_half<Key, K, T, true, true>(L, R, node(lo), threadIdx.x - HS::kThreads);
+            // ---- phase 2 ----
+            uint32_t used = (1u << ci) | (1u << li) | (1u << ri) | (merge_children ? (1u << hx) : 0u);
+            const int nxi = merge_cur ? free_buf(used) : ci;
+            used |= 1u << nxi;
+            const int li2 = free_buf(used);
+            used |= 1u << li2;
+            const int ri2 = free_buf(used);
+            used |= 1u << ri2;
+            const int hx2 = free_buf(used);
+            bool h2 = false;
+            if constexpr (kSplit) {
+                if (threadIdx.x < kHalf) {
+                    if (merge_cur) cta_merge_half<Key, K, T, true, false>(cur_s, hdata, buf(nxi), threadIdx.x, kHalf);
+                    if (merge_children) {
+                        cta_merge_half<Key, K, T, true, true>(L, R, node(lo), threadIdx.x, kHalf);
+                        grp_sync(1, kHalf);
+                        if (leader() && lo_locked) lane_unlock(lo, lo_rel);
+                    }
+                } else {
+                    acquire_children(hi, buf(li2), buf(ri2), kHalf, kHalf, 2);
+                    // the next level's H, if its children interleave (the same
+                    // test the next level makes)
+                    const Key* L2 = buf(li2);
+                    const Key* R2 = buf(ri2);
+                    const bool e2 = !sh->lk || L2[0] == kMaxKey || !sh->rk || R2[0] == kMaxKey;
+                    if (!e2 && !(elide && !needs_merge_full<Key, K>(L2, R2)))
+                        cta_merge_half<Key, K, T, false, false>(L2, R2, buf(hx2), threadIdx.x - kHalf, kHalf);
                 }
+                __syncthreads();
+                const Key* L2 = buf(li2);
+                const Key* R2 = buf(ri2);
+                const bool e2 = !sh->lk || L2[0] == kMaxKey || !sh->rk || R2[0] == kMaxKey;
+                h2 = !e2 && !(elide && !needs_merge_full<Key, K>(L2, R2));
+                have = true;
+                li = li2;
+                ri = ri2;
             } else {
-                if (merge_cur) cta_merge_half<Key, K, T, true, false>(cur_s, hdata, buf(nxi), threadIdx.x);
-                if (merge_children) cta_merge_half<Key, K, T, true, true>(L, R, node(lo), threadIdx.x);
+                if (merge_cur) cta_merge_half<Key, K, T, true, false>(cur_s, hdata, buf(nxi), threadIdx.x, T);
+                if (merge_children) cta_merge_half<Key, K, T, true, true>(L, R, node(lo), threadIdx.x, T);
+                __syncthreads();
+                if (leader() && lo_locked && merge_children) lane_unlock(lo, lo_rel);
+                have = false;
+                li = free_buf(1u << nxi);
+                ri = free_buf((1u << nxi) | (1u << li));
             }
-            __syncthreads();
-            if (leader() && lo_locked && merge_children) lane_unlock(lo, lo_rel);
             pf_add(pfLvMerge, tl3 - tl2);
             pf_add(pfLvRel, now() - tl3);
+            hx = h2 ? hx2 : -1;
             cur = hi;
             cur_rel = hi_rel;
-            ci = next_ci;
+            ci = nxi;
         }
     }
 };
 
 template <typename Key, int K, int T>
-__global__ void __launch_bounds__(T) heap_ops_kernel(HeapView hv, RunView rv) {
+__global__ void __launch_bounds__(T, (512 / T > 0 ? 512 / T : 1)) heap_ops_kernel(HeapView hv, RunView rv) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ OpShared sh;
     HeapCta<Key, K, T> cta(hv, rv, smem_raw, &sh);
@@ -1223,7 +1358,7 @@ template <typename Key, int K>
 struct KernelCfg {
     static constexpr int kWant = K / BH_THREADS_DIV;
     static constexpr int kThreads = kWant < 32 ? 32 : (kWant > BH_THREADS_CAP ? BH_THREADS_CAP : kWant);
-    static constexpr uint32_t kSmem = 6u * K * sizeof(Key);
+    static constexpr uint32_t kSmem = 8u * K * sizeof(Key) + 64;  // + window over-read pad
 };
 
 }  // namespace bh

@@ -23,6 +23,8 @@ constexpr uint32_t kStateStride = 8;  // uint32 words
 // Root queue lock: one flag per waiter slot, each on its own 128-byte line.
 constexpr uint32_t kRootQueue = 4096;
 constexpr uint32_t kRootFlagStride = 32;  // uint32 words
+// Profile buffer: 32 counters + 4 debug words per CTA (up to 4096 CTAs).
+constexpr uint32_t kProfWords = 32 + 4 * 4096;
 
 // Debug-only protocol toggles (bh_create flags, not in the public header).
 constexpr uint32_t kDbgSeqRefill = 0x100;       // reference refill order in every delete

@@ -277,7 +277,8 @@ class GeneralizedHeap:
     PROFILE_FIELDS = ("ins_ops", "ins_sort", "ins_root_wait", "ins_root_hold", "ins_rest",
                       "del_ops", "del_root_wait", "del_root_hold", "del_rest", "child_wait",
                       "levels", "cta_cycles", "rs_head", "rs_child", "rs_last", "rs_load",
-                      "rs_fill", "lv_acq", "lv_load", "lv_merge", "lv_rel")
+                      "rs_fill", "lv_acq", "lv_load", "lv_merge", "lv_rel", "served",
+                      "serve_holds", "bu_parent", "bu_retake", "bu_levels")
 
     def profile(self, reset: bool = True) -> dict:
         """SM-cycle profile of a BH_FLAG_PROFILE heap (see bh_profile)."""

@@ -65,4 +65,7 @@ for k in a.k:
                 print(f"   del root step us: head {us(p['rs_head'], d):.2f} child {us(p['rs_child'], d):.2f} last {us(p['rs_last'], d):.2f} "
                       f"load {us(p['rs_load'], d):.2f} fill {us(p['rs_fill'], d):.2f} | per level us: acq {us(p['lv_acq'], lv):.2f} "
                       f"load {us(p['lv_load'], lv):.2f} merge {us(p['lv_merge'], p['levels']):.2f} rel {us(p['lv_rel'], p['levels']):.2f}", flush=True)
+                bl = max(p['bu_levels'], 1)
+                print(f"   insert combining: served {p['served']} in {p['serve_holds']} holds | climb levels/ins {p['bu_levels']/max(p['ins_ops'],1):.2f} "
+                      f"parent-claim us {us(p['bu_parent'], bl):.2f} retake us {us(p['bu_retake'], bl):.2f}", flush=True)
             heap.close()
