@@ -208,6 +208,74 @@ BH_API uint64_t bh_bit_reverse(uint64_t x, unsigned bits);
  * Writes 64-bit keys, or 32-bit when key_bits == 32. */
 BH_API int bh_generate_keys(int order, uint64_t n, uint64_t seed, uint32_t key_bits, void* out);
 
+/* ---------------------------------------------------------------------------
+ * Application drivers: the reference's SSSP and knapsack
+ * branch-and-bound on the device heap.  Host buffers in and out; every
+ * per-node step (heap ops, relaxation, child expansion) runs on `device`.
+ * ------------------------------------------------------------------------- */
+/* grid_graph(rows, cols, seed) (proj/src/graph.cpp:174-193) in the CSR layout
+ * of Graph::Graph (graph.cpp:12-30): offsets[rows*cols+1], and per arc the
+ * target node and weight (uniform [1,1000] from mt19937_64(seed)). */
+BH_API uint64_t bh_grid_graph_edges(uint32_t rows, uint32_t cols);
+BH_API int bh_grid_graph(uint32_t rows, uint32_t cols, uint64_t seed, uint64_t* offsets,
+                         uint32_t* adj_node, uint32_t* adj_weight);
+
+/* SsspConfig (proj/include/batchheap/sssp.hpp:27-31); the reference's host
+ * workers become the heap's persistent CTAs (0 = all co-resident). */
+typedef struct {
+    uint64_t threshold;          /* active-set size that engages the heap (0 -> 10000) */
+    uint32_t heap_node_capacity; /* k (0 -> 1024; the reference uses 32) */
+    uint32_t ctas;
+    uint64_t reserved;
+} bh_sssp_cfg;
+typedef struct {
+    uint64_t visits;            /* SsspResult::visits: non-stale explorations */
+    uint64_t rounds;
+    uint64_t keys_through_heap; /* keys funnelled through the heap */
+    double seconds;
+} bh_sssp_stats;
+/* sssp(graph, source, config) (proj/src/sssp.cpp:118-194).  dist: n_nodes
+ * distances, UINT64_MAX where unreachable; BH_E_INVALID_KEY when a distance
+ * exceeds the key encoding (sssp.cpp:16-20 overflow_error). */
+BH_API int bh_sssp(uint32_t n_nodes, const uint64_t* offsets, const uint32_t* adj_node,
+                   const uint32_t* adj_weight, uint32_t source, const bh_sssp_cfg* cfg, int device,
+                   uint64_t* dist, bh_sssp_stats* stats);
+
+/* KnapsackType (proj/include/batchheap/knapsack.hpp:16-21). */
+enum {
+    BH_KS_STRONGLY_CORRELATED = 0,
+    BH_KS_ALMOST_STRONGLY_CORRELATED = 1,
+    BH_KS_EVEN_ODD = 2,
+    BH_KS_SUBSET_SUM = 3
+};
+/* generate_knapsack(type, n, range, seed) (proj/src/knapsack.cpp:22-66):
+ * fills weight[n], benefit[n]; returns the capacity (0 on bad arguments). */
+BH_API uint64_t bh_generate_knapsack(int type, uint32_t n, uint32_t range, uint64_t seed,
+                                     uint32_t* weight, uint32_t* benefit);
+/* BbConfig (knapsack.hpp:56-60) plus the device round shape. */
+typedef struct {
+    uint64_t gc_threshold;       /* keys; 0 disables GC (reference 1 << 16) */
+    uint32_t heap_node_capacity; /* k (0 -> 1024; the reference uses 32) */
+    uint32_t ctas;               /* persistent CTAs (0 = all co-resident) */
+    uint32_t pop_ops;            /* deleteMin batches per round (0 -> 4) */
+    uint32_t reserved;
+    uint64_t arena_nodes;        /* branch-and-bound node arena (0 -> 1 << 28) */
+} bh_bb_cfg;
+/* BbOutcome (knapsack.hpp:62-66) plus round statistics. */
+typedef struct {
+    uint64_t best;
+    uint64_t explored;
+    uint64_t gc_passes;
+    uint64_t rounds;
+    uint64_t arena_nodes;
+    double seconds;
+} bh_bb_outcome;
+/* knapsack_bb(instance, config) (proj/src/knapsack.cpp:206-368): the
+ * optimum of the 0/1 knapsack; BH_E_CAPACITY when the node arena is
+ * exhausted (the reference's "branch-and-bound arena exhausted"). */
+BH_API int bh_knapsack_bb(uint32_t n, const uint32_t* weight, const uint32_t* benefit, uint64_t capacity,
+                          const bh_bb_cfg* cfg, int device, bh_bb_outcome* out);
+
 /* Library build identity (sm arch, compile flags). */
 BH_API const char* bh_build_info(void);
 

@@ -282,6 +282,8 @@ def ref():
         r.ref_generate_knapsack.restype = C.c_uint64
         r.ref_knapsack_dp.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64]
         r.ref_knapsack_dp.restype = C.c_uint64
+        r.ref_knapsack_bb.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64,
+                                      C.c_uint32, _u64p, C.POINTER(C.c_double)]
         _ref = r
     return _ref
 
@@ -293,6 +295,31 @@ def ref_phase(variant: int, k: int, n_keys: int, workers: int, seed: int = 1, ve
     if st != 0:
         raise RuntimeError(f"ref_phase failed ({st}): {ref().ref_last_error().decode()}")
     return float(t[0]), float(t[1])
+
+
+def ref_knapsack_bb_subprocess(kind: int, n: int, rng_range: int, seed: int, workers: int = 2,
+                               gc_threshold: int = 1 << 16, k: int = 32, timeout: float = 120.0) -> dict:
+    """The reference's knapsack_bb in a child process (an arena exhaustion
+    terminates the process, knapsack.cpp:136-154): {best, explored, gc,
+    seconds} or {error}."""
+    import subprocess
+    import sys
+    code = (f"import sys; sys.path.insert(0, {os.path.dirname(HERE)!r});"
+            "import ctypes as C, numpy as np; from oracle import oracle as O;"
+            "o = np.zeros(3, np.uint64); t = C.c_double();"
+            f"st = O.ref().ref_knapsack_bb({kind}, {n}, {rng_range}, {seed}, {workers}, {gc_threshold}, {k}, o,"
+            " C.byref(t));"
+            "print(st, int(o[0]), int(o[1]), int(o[2]), t.value)")
+    try:
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=timeout)
+    except subprocess.TimeoutExpired:
+        return {"error": f"timeout {timeout}s"}
+    if r.returncode != 0 or not r.stdout.strip():
+        return {"error": f"terminated (rc {r.returncode}): {r.stderr.strip()[-160:]}"}
+    st, best, explored, gc, secs = r.stdout.split()
+    if int(st) != 0:
+        return {"error": f"status {st}"}
+    return {"best": int(best), "explored": int(explored), "gc": int(gc), "seconds": float(secs)}
 
 
 class RefHeap:

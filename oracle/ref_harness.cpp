@@ -278,4 +278,26 @@ std::uint64_t ref_knapsack_dp(int type, std::uint32_t n, std::uint32_t range, st
     return knapsack_dp(generate_knapsack(static_cast<KnapsackType>(type), n, range, seed));
 }
 
+// The reference's branch-and-bound (proj/src/knapsack.cpp:206-368).  An
+// arena exhaustion inside a worker thread calls std::terminate in the
+// reference: callers run this in a child process.  out3 = best, explored,
+// gc passes.
+int ref_knapsack_bb(int type, std::uint32_t n, std::uint32_t range, std::uint64_t seed, std::uint32_t workers,
+                    std::uint64_t gc_threshold, std::uint32_t k, std::uint64_t* out3, double* seconds) {
+    return guarded([&] {
+        auto inst = generate_knapsack(static_cast<KnapsackType>(type), n, range, seed);
+        BbConfig cfg;
+        cfg.workers = workers;
+        cfg.gc_threshold = gc_threshold;
+        cfg.heap_node_capacity = k;
+        auto t0 = std::chrono::steady_clock::now();
+        auto o = knapsack_bb(inst, cfg);
+        auto t1 = std::chrono::steady_clock::now();
+        out3[0] = o.best;
+        out3[1] = o.explored;
+        out3[2] = o.gc_passes;
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
 }  // extern "C"

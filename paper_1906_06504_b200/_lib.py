@@ -44,6 +44,26 @@ class bh_run_cfg(C.Structure):
     _fields_ = [("ctas", C.c_uint32), ("flags", C.c_uint32), ("stream", C.c_void_p)]
 
 
+class bh_sssp_cfg(C.Structure):
+    _fields_ = [("threshold", C.c_uint64), ("heap_node_capacity", C.c_uint32), ("ctas", C.c_uint32),
+                ("reserved", C.c_uint64)]
+
+
+class bh_sssp_stats(C.Structure):
+    _fields_ = [("visits", C.c_uint64), ("rounds", C.c_uint64), ("keys_through_heap", C.c_uint64),
+                ("seconds", C.c_double)]
+
+
+class bh_bb_cfg(C.Structure):
+    _fields_ = [("gc_threshold", C.c_uint64), ("heap_node_capacity", C.c_uint32), ("ctas", C.c_uint32),
+                ("pop_ops", C.c_uint32), ("reserved", C.c_uint32), ("arena_nodes", C.c_uint64)]
+
+
+class bh_bb_outcome(C.Structure):
+    _fields_ = [("best", C.c_uint64), ("explored", C.c_uint64), ("gc_passes", C.c_uint64),
+                ("rounds", C.c_uint64), ("arena_nodes", C.c_uint64), ("seconds", C.c_double)]
+
+
 class bh_event(C.Structure):
     _fields_ = [("ts", C.c_uint64), ("op", C.c_uint32), ("kind", C.c_uint16),
                 ("pad", C.c_uint16), ("node", C.c_uint64)]
@@ -77,6 +97,11 @@ SIGNATURES = {
     "bh_bit_reverse": (_u64, [_u64, C.c_uint]),
     "bh_generate_keys": (_i, [_i, _u64, _u64, _u32, _vp]),
     "bh_build_info": (C.c_char_p, []),
+    "bh_grid_graph_edges": (_u64, [_u32, _u32]),
+    "bh_grid_graph": (_i, [_u32, _u32, _u64, _vp, _vp, _vp]),
+    "bh_sssp": (_i, [_u32, _vp, _vp, _vp, _u32, C.POINTER(bh_sssp_cfg), _i, _vp, C.POINTER(bh_sssp_stats)]),
+    "bh_generate_knapsack": (_u64, [_i, _u32, _u32, _u64, _vp, _vp]),
+    "bh_knapsack_bb": (_i, [_u32, _vp, _vp, _u64, C.POINTER(bh_bb_cfg), _i, C.POINTER(bh_bb_outcome)]),
 }
 
 _lib = None

@@ -63,6 +63,12 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+}  // namespace
+
+extern "C" int bh_internal_fail(int code, const char* msg) { return fail(code, msg ? msg : ""); }
+
+namespace {
+
 int cuda_fail(cudaError_t e, const char* where) {
     return fail(BH_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }

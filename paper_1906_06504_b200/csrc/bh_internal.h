@@ -119,6 +119,9 @@ struct KernelInfo {
 
 }  // namespace bh
 
+// Sets the thread-local bh_last_error() message (bh_capi.cu); returns code.
+extern "C" int bh_internal_fail(int code, const char* msg);
+
 // Device-side dispatch implemented in bh_kernels_*.cu.
 extern "C" int bh_internal_launch_ops(uint32_t key_bits, const bh::HeapView* hv, const bh::RunView* rv,
                                       uint32_t ctas, void* stream);

@@ -1,0 +1,9 @@
+# bench line + reference arm + ncu evidence (launch list of the bench command,
+# one --set full capture of the deleteMin launch)
+mkdir -p gpurun_out/r02
+timeout 600 python bench.py > gpurun_out/r02/bench.json 2> gpurun_out/r02/bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/r02/bench_ref.json 2> gpurun_out/r02/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r02/b_ncu.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:heap_ops_kernel --launch-skip 1 -c 1 -o gpurun_out/r02/full_delete -f python tools/probe_phase.py --log2n 26 --k 1024 > gpurun_out/r02/full.log 2>&1
+tail -3 gpurun_out/r02/full.log
+cat gpurun_out/r02/bench.json gpurun_out/r02/bench_ref.json
