@@ -259,7 +259,8 @@ typedef struct {
     uint32_t ctas;               /* persistent CTAs (0 = all co-resident) */
     uint32_t pop_ops;            /* deleteMin batches per round (0 -> 4) */
     uint32_t reserved;
-    uint64_t arena_nodes;        /* branch-and-bound node arena (0 -> 1 << 28) */
+    uint64_t arena_nodes;        /* node slots (recycled; 0 -> 1 << 28) */
+    uint64_t max_explored;       /* node budget: BH_E_CAPACITY past it (0 -> 1 << 29) */
 } bh_bb_cfg;
 /* BbOutcome (knapsack.hpp:62-66) plus round statistics. */
 typedef struct {
@@ -271,8 +272,9 @@ typedef struct {
     double seconds;
 } bh_bb_outcome;
 /* knapsack_bb(instance, config) (proj/src/knapsack.cpp:206-368): the
- * optimum of the 0/1 knapsack; BH_E_CAPACITY when the node arena is
- * exhausted (the reference's "branch-and-bound arena exhausted"). */
+ * optimum of the 0/1 knapsack; BH_E_CAPACITY when the node slots or the
+ * node budget run out (the reference's "branch-and-bound arena exhausted",
+ * which it raises inside a worker and terminates on). */
 BH_API int bh_knapsack_bb(uint32_t n, const uint32_t* weight, const uint32_t* benefit, uint64_t capacity,
                           const bh_bb_cfg* cfg, int device, bh_bb_outcome* out);
 

@@ -56,7 +56,8 @@ class bh_sssp_stats(C.Structure):
 
 class bh_bb_cfg(C.Structure):
     _fields_ = [("gc_threshold", C.c_uint64), ("heap_node_capacity", C.c_uint32), ("ctas", C.c_uint32),
-                ("pop_ops", C.c_uint32), ("reserved", C.c_uint32), ("arena_nodes", C.c_uint64)]
+                ("pop_ops", C.c_uint32), ("reserved", C.c_uint32), ("arena_nodes", C.c_uint64),
+                ("max_explored", C.c_uint64)]
 
 
 class bh_bb_outcome(C.Structure):

@@ -134,7 +134,9 @@ def generate_knapsack(kind: KnapsackType, n: int, rng_range: int, seed: int) -> 
 class BbConfig:
     """BbConfig (knapsack.hpp:56-60): ``gc_threshold`` and
     ``heap_node_capacity`` as the reference; ``ctas`` replaces workers; a
-    round pops ``pop_ops`` batches; ``arena_nodes`` bounds the node arena.
+    round pops ``pop_ops`` batches; ``arena_nodes`` node slots (recycled
+    once a node is expanded or dropped) and ``max_explored`` (the node
+    budget) bound a run.
     Defaults tuned on the device (tools/apps_sweep.py; the reference uses
     k = 32 and GC at 2^16 keys); the optimum does not depend on them."""
     gc_threshold: int = 1 << 20
@@ -142,6 +144,7 @@ class BbConfig:
     ctas: int = 0
     pop_ops: int = 4
     arena_nodes: int = 1 << 28
+    max_explored: int = 1 << 29
 
 
 @dataclasses.dataclass
@@ -157,9 +160,10 @@ class BbOutcome:
 
 def knapsack_bb(instance: KnapsackInstance, config: Optional[BbConfig] = None, device: int = 0) -> BbOutcome:
     """knapsack_bb(instance, config) (proj/src/knapsack.cpp:206-368) on the
-    GPU.  Raises CapacityError when the node arena is exhausted."""
+    GPU.  Raises CapacityError when the node slots or budget run out."""
     cfg = config or BbConfig()
-    c = L.bh_bb_cfg(cfg.gc_threshold, cfg.heap_node_capacity, cfg.ctas, cfg.pop_ops, 0, cfg.arena_nodes)
+    c = L.bh_bb_cfg(cfg.gc_threshold, cfg.heap_node_capacity, cfg.ctas, cfg.pop_ops, 0, cfg.arena_nodes,
+                    cfg.max_explored)
     o = L.bh_bb_outcome()
     w = np.ascontiguousarray(instance.weight, dtype=np.uint32)
     b = np.ascontiguousarray(instance.benefit, dtype=np.uint32)

@@ -188,17 +188,60 @@ struct BbDev {
     unsigned long long* best;
     unsigned long long* explored;
     unsigned long long* err;  // 1 = arena exhausted
+    // Recycled slots: a stack of free handles.  The reference never frees
+    // (its arena fills and the run terminates, knapsack.cpp:136-154); here
+    // a popped node is dead once expanded (its children copy what they
+    // need), so its slot is reused.  free_n is the stack height at kernel
+    // start (fixed during a kernel), free_taken counts pops from the top.
+    uint32_t* free_stack;
+    unsigned long long* free_n;
+    unsigned long long* free_taken;
+    unsigned long long* free_pushed;
 };
 
 __device__ bool bb_alloc(const BbDev& d, const BbNode& node, uint32_t& handle) {
-    const unsigned long long h = atomicAdd(d.arena_next, 1ull);
-    if (h >= d.arena_cap) {
-        atomicOr(d.err, 1ull);
-        return false;
+    const unsigned long long avail = *d.free_n;
+    unsigned long long h;
+    const unsigned long long idx = avail ? atomicAdd(d.free_taken, 1ull) : avail;
+    if (idx < avail) {
+        h = d.free_stack[avail - 1 - idx];
+    } else {
+        h = atomicAdd(d.arena_next, 1ull);
+        if (h >= d.arena_cap) {
+            atomicOr(d.err, 1ull);
+            return false;
+        }
     }
     d.arena[h] = node;
     handle = (uint32_t)h;
     return true;
+}
+
+// After a round: push the handles of every popped key (keep == nullptr) or
+// of the drained keys GC dropped onto the free stack, above what the round
+// left of it; bb_free_finish then settles the height.
+__global__ void bb_free_popped(BbDev d, const unsigned long long* out, const uint32_t* lens, unsigned long long n_ops,
+                               uint32_t k, bool gc_drop_only) {
+    const unsigned long long total = n_ops * k;
+    const unsigned long long avail = *d.free_n;
+    const unsigned long long used = min(*d.free_taken, avail);
+    const unsigned long long base = avail - used;
+    const unsigned long long best_now = *d.best;
+    for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; t < total;
+         t += (unsigned long long)gridDim.x * blockDim.x) {
+        if ((uint32_t)(t % k) >= lens[t / k]) continue;
+        const uint32_t h = (uint32_t)out[t];
+        if (gc_drop_only && d.arena[h].bound > best_now) continue;  // kept by GC
+        d.free_stack[base + atomicAdd(d.free_pushed, 1ull)] = h;
+    }
+}
+
+__global__ void bb_free_finish(BbDev d) {
+    const unsigned long long avail = *d.free_n;
+    const unsigned long long used = min(*d.free_taken, avail);
+    *d.free_n = avail - used + *d.free_pushed;
+    *d.free_taken = 0;
+    *d.free_pushed = 0;
 }
 
 // The worker loop body (knapsack.cpp:293-337) for every popped key: prune,
@@ -468,7 +511,8 @@ int bh_knapsack_bb(uint32_t n, const uint32_t* weight, const uint32_t* benefit, 
     // defaults tuned for the device (tools/apps_sweep.py): k = 1024, four
     // batches per round, GC at 2^20 keys (reference: k = 32, 2 workers, GC
     // at 2^16); the optimum does not depend on them
-    bh_bb_cfg cfg = cfg_in ? *cfg_in : bh_bb_cfg{1u << 20, 1024, 0, 4, 0, 0};
+    bh_bb_cfg cfg = cfg_in ? *cfg_in : bh_bb_cfg{1u << 20, 1024, 0, 4, 0, 0, 0};
+    if (cfg.max_explored == 0) cfg.max_explored = 1ull << 29;
     if (cfg.heap_node_capacity == 0) cfg.heap_node_capacity = 1024;
     if (cfg.pop_ops == 0) cfg.pop_ops = 4;
     if (cfg.arena_nodes == 0) cfg.arena_nodes = 1ull << 28;  // 4 GiB of 16-byte nodes
@@ -515,10 +559,12 @@ int bh_knapsack_bb(uint32_t n, const uint32_t* weight, const uint32_t* benefit, 
     APP_OK(d_sw.alloc(n));
     APP_OK(d_sb.alloc(n));
     APP_OK(d_arena.alloc(cfg.arena_nodes));
-    APP_OK(d_ctr.alloc(8));  // 0 arena_next, 1 best, 2 explored, 3 err, 4 key count
+    DevBuf<uint32_t> d_free;
+    APP_OK(d_free.alloc(cfg.arena_nodes));
+    APP_OK(d_ctr.alloc(8));  // 0 arena_next, 1 best, 2 explored, 3 err, 4 key count, 5-7 free stack
     APP_CUDA(cudaMemcpyAsync(d_sw.p, sw.data(), n * 4, cudaMemcpyHostToDevice, s));
     APP_CUDA(cudaMemcpyAsync(d_sb.p, sb.data(), n * 4, cudaMemcpyHostToDevice, s));
-    unsigned long long init[8] = {1, 0, 0, 0, 1, 0, 0, 0};
+    unsigned long long init[8] = {1, 0, 0, 0, 1, 0, 0, 0};  // arena slot 0 = the root
     APP_CUDA(cudaMemcpyAsync(d_ctr.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
     const BbNode root{0, 0, 0, (uint32_t)root_bound};
     APP_CUDA(cudaMemcpyAsync(d_arena.p, &root, sizeof(root), cudaMemcpyHostToDevice, s));
@@ -535,7 +581,8 @@ int bh_knapsack_bb(uint32_t n, const uint32_t* weight, const uint32_t* benefit, 
     HeapRunner hr{hg.h, s, k, cfg.ctas};
     APP_OK(d_keys.alloc(std::max<uint64_t>(2 * pop_keys, 1024)));
     APP_OK(d_out.alloc(pop_keys));
-    BbDev dv{d_sw.p, d_sb.p, n, capacity, d_arena.p, cfg.arena_nodes, d_ctr.p, d_ctr.p + 1, d_ctr.p + 2, d_ctr.p + 3};
+    BbDev dv{d_sw.p,      d_sb.p,      n,           capacity,   d_arena.p,  cfg.arena_nodes, d_ctr.p, d_ctr.p + 1,
+             d_ctr.p + 2, d_ctr.p + 3, d_free.p,   d_ctr.p + 5, d_ctr.p + 6, d_ctr.p + 7};
 
     // the root key
     {
@@ -552,9 +599,13 @@ int bh_knapsack_bb(uint32_t n, const uint32_t* weight, const uint32_t* benefit, 
         APP_OK(hr.run(1, n_del * k, nullptr, d_out.p));
         bb_expand<<<grid_for(n_del * k), 256, 0, s>>>(dv, d_out.p, hr.lens.p, n_del, k, d_keys.p, d_ctr.p + 4);
         APP_CUDA(cudaGetLastError());
+        bb_free_popped<<<grid_for(n_del * k), 256, 0, s>>>(dv, d_out.p, hr.lens.p, n_del, k, false);
+        bb_free_finish<<<1, 1, 0, s>>>(dv);
+        APP_CUDA(cudaGetLastError());
         APP_CUDA(cudaMemcpyAsync(h_ctr, d_ctr.p, 8 * 8, cudaMemcpyDeviceToHost, s));
         APP_CUDA(cudaStreamSynchronize(s));
         if (h_ctr[3]) return fail(BH_E_CAPACITY, "branch-and-bound arena exhausted");
+        if (h_ctr[2] > cfg.max_explored) return fail(BH_E_CAPACITY, "branch-and-bound node budget exhausted");
         const uint64_t pushed = h_ctr[4];
         APP_OK(hr.run(0, pushed, d_keys.p, nullptr));
         bh_peek pk;
@@ -571,6 +622,8 @@ int bh_knapsack_bb(uint32_t n, const uint32_t* weight, const uint32_t* benefit, 
             APP_OK(hr.run(1, drain_ops * k, nullptr, d_out.p));
             bb_gc_filter<<<grid_for(drain_ops * k), 256, 0, s>>>(dv, d_out.p, hr.lens.p, drain_ops, k, d_keys.p,
                                                                   d_ctr.p + 4);
+            bb_free_popped<<<grid_for(drain_ops * k), 256, 0, s>>>(dv, d_out.p, hr.lens.p, drain_ops, k, true);
+            bb_free_finish<<<1, 1, 0, s>>>(dv);
             APP_CUDA(cudaGetLastError());
             APP_CUDA(cudaMemcpyAsync(h_ctr + 4, d_ctr.p + 4, 8, cudaMemcpyDeviceToHost, s));
             APP_CUDA(cudaStreamSynchronize(s));
@@ -587,7 +640,7 @@ int bh_knapsack_bb(uint32_t n, const uint32_t* weight, const uint32_t* benefit, 
     outcome->explored = h_ctr[2];
     outcome->gc_passes = gc_passes;
     outcome->rounds = rounds;
-    outcome->arena_nodes = h_ctr[0];
+    outcome->arena_nodes = h_ctr[0];  // slots ever used (high-water mark)
     outcome->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return BH_OK;
 }

@@ -51,10 +51,10 @@ def test_sssp_grid_2048_golden_source0():
     assert A.dist_summary(r.dist) == {k: case[k] for k in ("sum", "max", "unreachable")}
 
 
-# Golden instances (all four families) whose branch-and-bound exhausts the
-# node arena on the GPU too (the reference terminates on a superset of
-# these, tests/golden/knapsack_ref_bb_w1.json), and the ones that take
-# seconds.
+# Golden instances (all four families) whose branch-and-bound exceeds the
+# default node budget (2^29 nodes) on the GPU too -- the reference
+# terminates on a superset of these, tests/golden/knapsack_ref_bb_w1.json --
+# and the ones that take seconds.
 EXHAUST = {(0, 100, 1000, 3), (0, 200, 1000, 2), (0, 200, 7000, 2), (1, 200, 1000, 1), (1, 200, 7000, 1),
            (2, 200, 1000, 1), (2, 200, 1000, 3), (2, 200, 7000, 1)}
 SLOW = {(0, 100, 1000, 1), (0, 100, 7000, 1), (1, 100, 1000, 1), (1, 100, 7000, 1), (1, 200, 7000, 2),
@@ -95,8 +95,10 @@ def test_knapsack_bb_arena_exhaustion_raises():
     136-154) is a CapacityError here instead of std::terminate."""
     from paper_1906_06504_b200 import CapacityError
     inst = A.generate_knapsack(A.KnapsackType.StronglyCorrelated, 200, 1000, 2)
-    with pytest.raises(CapacityError):
-        A.knapsack_bb(inst, A.BbConfig(arena_nodes=1 << 20))
+    with pytest.raises(CapacityError, match="budget"):
+        A.knapsack_bb(inst, A.BbConfig(max_explored=1 << 20))
+    with pytest.raises(CapacityError, match="arena"):
+        A.knapsack_bb(inst, A.BbConfig(arena_nodes=1 << 12))
 
 
 @pytest.mark.parametrize("k,pop", [(32, 1), (32, 64), (256, 16)])
