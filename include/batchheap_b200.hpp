@@ -165,6 +165,94 @@ class GeneralizedHeap {
     std::uint32_t max_nodes_;
 };
 
+// ---- drivers (proj/include/batchheap/{graph,sssp,knapsack}.hpp) --------
+inline constexpr std::uint64_t kUnreachable = ~std::uint64_t{0};  // sssp.hpp:18-19
+
+struct Graph {  // graph.hpp:26-50, CSR
+    std::vector<std::uint64_t> offsets;
+    std::vector<std::uint32_t> nbr;
+    std::vector<std::uint32_t> weight;
+    std::uint32_t node_count() const { return static_cast<std::uint32_t>(offsets.size() - 1); }
+    std::uint64_t edge_count() const { return nbr.size(); }
+};
+
+inline Graph grid_graph(std::uint32_t rows, std::uint32_t cols, std::uint64_t seed) {  // graph.cpp:174-193
+    Graph g;
+    const std::uint64_t m = bh_grid_graph_edges(rows, cols);
+    g.offsets.resize(std::uint64_t{rows} * cols + 1);
+    g.nbr.resize(m);
+    g.weight.resize(m);
+    detail::check(bh_grid_graph(rows, cols, seed, g.offsets.data(), g.nbr.data(), g.weight.data()));
+    return g;
+}
+
+struct SsspConfig {  // sssp.hpp:27-31 (workers -> persistent CTAs; k default 1024 on the device)
+    std::uint64_t threshold = 10'000;
+    std::uint32_t ctas = 0;
+    std::uint32_t heap_node_capacity = 1024;
+};
+
+struct SsspResult {  // sssp.hpp:21-24
+    std::vector<std::uint64_t> dist;
+    std::uint64_t visits = 0;
+};
+
+inline SsspResult sssp(const Graph& g, std::uint32_t source, const SsspConfig& config = {}, int device = 0) {
+    SsspResult r;
+    r.dist.resize(g.node_count());
+    bh_sssp_cfg c{config.threshold, config.heap_node_capacity, config.ctas, 0};
+    bh_sssp_stats st{};
+    detail::check(bh_sssp(g.node_count(), g.offsets.data(), g.nbr.data(), g.weight.data(), source, &c, device,
+                          r.dist.data(), &st));
+    r.visits = st.visits;
+    return r;
+}
+
+enum class KnapsackType { StronglyCorrelated, AlmostStronglyCorrelated, EvenOdd, SubsetSum };  // knapsack.hpp:16
+
+struct KnapsackInstance {  // knapsack.hpp:23-31
+    KnapsackType type = KnapsackType::SubsetSum;
+    std::uint32_t n = 0;
+    std::uint32_t range = 0;
+    std::vector<std::uint32_t> weight;
+    std::vector<std::uint32_t> benefit;
+    std::uint64_t capacity = 0;
+};
+
+inline KnapsackInstance generate_knapsack(KnapsackType type, std::uint32_t n, std::uint32_t range,
+                                          std::uint64_t seed) {  // knapsack.cpp:22-66
+    KnapsackInstance inst;
+    inst.type = type;
+    inst.n = n;
+    inst.range = range;
+    inst.weight.resize(n);
+    inst.benefit.resize(n);
+    inst.capacity =
+        bh_generate_knapsack(static_cast<int>(type), n, range, seed, inst.weight.data(), inst.benefit.data());
+    if (inst.capacity == 0) detail::check(BH_E_CONFIG);
+    return inst;
+}
+
+struct BbConfig {  // knapsack.hpp:56-60 (device defaults: k 1024, GC at 2^20)
+    std::uint32_t ctas = 0;
+    std::uint64_t gc_threshold = 1 << 20;
+    std::uint32_t heap_node_capacity = 1024;
+    std::uint32_t pop_ops = 4;
+};
+
+struct BbOutcome {  // knapsack.hpp:62-66
+    std::uint64_t best = 0;
+    std::uint64_t explored = 0;
+    std::uint64_t gc_passes = 0;
+};
+
+inline BbOutcome knapsack_bb(const KnapsackInstance& inst, const BbConfig& config = {}, int device = 0) {
+    bh_bb_cfg c{config.gc_threshold, config.heap_node_capacity, config.ctas, config.pop_ops, 0, 0, 0};
+    bh_bb_outcome o{};
+    detail::check(bh_knapsack_bb(inst.n, inst.weight.data(), inst.benefit.data(), inst.capacity, &c, device, &o));
+    return {o.best, o.explored, o.gc_passes};
+}
+
 // Bit-reversal target selection (proj/include/batchheap/bitrev.hpp).
 inline std::uint64_t slot_for_rank(std::uint64_t rank) { return bh_slot_for_rank(rank); }
 inline std::uint64_t bit_reverse(std::uint64_t x, unsigned bits) { return bh_bit_reverse(x, bits); }

@@ -2,6 +2,7 @@
 // unchanged in shape through batchheap_b200::GeneralizedHeap.  Built by
 // tests/test_cpp_facade.py; exits non-zero on the first failed check.
 #include <algorithm>
+#include <queue>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -120,6 +121,38 @@ int main() {
         for (int i = 0; i < 4; ++i) {
             heap.insert(std::vector<Key>{Key(2 * i + 1), Key(2 * i + 2)});
             CHECK(heap.select_insert_target() == expect[i]);
+        }
+    }
+    {  // drivers in the reference's call shape (batchheap_main.cpp:192, :239-246):
+       // SSSP vs a textbook Dijkstra, B&B vs the DP optimum
+        const Graph g = grid_graph(40, 30, 3);
+        auto r = sssp(g, 7, SsspConfig{64, 0, 32});
+        std::vector<std::uint64_t> d(g.node_count(), kUnreachable);
+        using Item = std::pair<std::uint64_t, std::uint32_t>;
+        std::priority_queue<Item, std::vector<Item>, std::greater<>> q;
+        d[7] = 0;
+        q.push({0, 7});
+        while (!q.empty()) {
+            auto [du, u] = q.top();
+            q.pop();
+            if (du != d[u]) continue;
+            for (std::uint64_t a = g.offsets[u]; a < g.offsets[u + 1]; ++a) {
+                const std::uint64_t c = du + g.weight[a];
+                if (c < d[g.nbr[a]]) {
+                    d[g.nbr[a]] = c;
+                    q.push({c, g.nbr[a]});
+                }
+            }
+        }
+        CHECK(r.dist == d);
+        CHECK(throws<ConfigError>([&] { sssp(g, g.node_count()); }));
+        for (auto t : {KnapsackType::StronglyCorrelated, KnapsackType::SubsetSum}) {
+            const auto inst = generate_knapsack(t, 40, 1000, 5);
+            std::vector<std::uint64_t> table(inst.capacity + 1, 0);
+            for (std::uint32_t i = 0; i < inst.n; ++i)
+                for (std::uint64_t c = inst.capacity; c >= inst.weight[i]; --c)
+                    table[c] = std::max(table[c], table[c - inst.weight[i]] + inst.benefit[i]);
+            CHECK(knapsack_bb(inst).best == table[inst.capacity]);
         }
     }
     std::printf("facade: %d failures\n", failures);
