@@ -75,6 +75,13 @@ __device__ __forceinline__ void state_release(uint32_t* p, uint32_t from, uint32
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(delta) : "memory");
 }
 
+// The same transition without release semantics, for a hand-off that
+// publishes no data (the gated BU park).
+__device__ __forceinline__ void state_release_relaxed(uint32_t* p, uint32_t from, uint32_t to) {
+    const uint32_t delta = 8u + to - from;
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(delta) : "memory");
+}
+
 // Warm L2 with n bytes at p (one prefetch per 128-byte line), issued by
 // threads [first, first + lines).  A hint only: the later ld.cg of the lock
 // holder reads whatever L2 holds then.

@@ -51,6 +51,7 @@ struct OpShared {
     unsigned long long plen;
     unsigned long long seq;
     unsigned long long deleters;
+    unsigned long long root_tk;  // ticket under which this CTA holds the root
     uint32_t act;
     uint32_t cw[3];     // observed state words (children / claimed node)
     uint32_t claim[3];  // 1 = claimable, 0 = skip (empty)
@@ -126,7 +127,6 @@ struct HeapCta {
     unsigned long long cnt[kNumCounters];
     unsigned long long pf[kNumProf];
     unsigned long long cur_op;
-    unsigned long long root_ticket;
     bool elide;
     bool record;
     bool prof;
@@ -143,7 +143,6 @@ struct HeapCta {
         for (int i = 0; i < kNumCounters; ++i) cnt[i] = 0;
 #pragma unroll
         for (int i = 0; i < kNumProf; ++i) pf[i] = 0;
-        root_ticket = 0;
         elide = (h.flags & BH_FLAG_ELIDE_MERGES) != 0;
         record = (h.flags & BH_FLAG_RECORD) != 0;
         prof = h.prof != nullptr;
@@ -245,14 +244,14 @@ struct HeapCta {
         Backoff b;
         uint32_t v;
         while (((v = state_load(f)) & ~1u) != granted) { b.pause(); BH_WAIT_NOTE(__LINE__); }
-        root_ticket = t;
+        sh->root_tk = t;
         if (v & 1u) return true;
         if (record_it) rec_lane(kEvAcq, 1);
         return false;
     }
     __device__ void root_unlock(bool record_it = true) {
         if (record_it) rec_lane(kEvRel, 1);
-        const unsigned long long nt = root_ticket + 1;
+        const unsigned long long nt = sh->root_tk + 1;
         state_store_release(qline(nt), (uint32_t)nt << 1);
     }
 
@@ -271,8 +270,7 @@ struct HeapCta {
         unsigned long long tail = 0;
         if (lane == 0) tail = ld_cg_u64(&hdr->root_tail);
         tail = __shfl_sync(0xFFFFFFFFu, tail, 0);
-        // root_ticket lives in the leader lane only
-        const unsigned long long mine = __shfl_sync(0xFFFFFFFFu, root_ticket, 0);
+        const unsigned long long mine = sh->root_tk;
         const unsigned long long t = mine + 1 + lane;
         uint32_t* f = qline(t);
         bool ok = t < tail && nodes_after + 1 + lane <= hv.max_nodes;
@@ -311,13 +309,14 @@ struct HeapCta {
 
     // Non-root claim: wait for one of `accept` (bitmask of states), CAS it to
     // INUSE.  Returns the state it was claimed from.  Calling lane only.
-    __device__ uint32_t lane_claim(unsigned long long slot, uint32_t accept) {
+    __device__ uint32_t lane_claim(unsigned long long slot, uint32_t accept, uint32_t* claimed_word = nullptr) {
         uint32_t* p = st(slot);
         Backoff b;
         for (;;) {
             const uint32_t w = state_load(p);
             if (((accept >> sget(w)) & 1u) && state_cas(p, w, swith(w, kInUse))) {
                 BH_OWN(slot);
+                if (claimed_word) *claimed_word = swith(w, kInUse);
                 return sget(w);
             }
             { b.pause(); BH_WAIT_NOTE(__LINE__); }
@@ -467,7 +466,7 @@ struct HeapCta {
             if (served) {
                 // a combiner ran the root phase: rank, claimed target, sequence
                 const unsigned long long* f =
-                    reinterpret_cast<const unsigned long long*>(qline(root_ticket));
+                    reinterpret_cast<const unsigned long long*>(qline(sh->root_tk));
                 sh->nodes = ld_cg_u64(f + 2) - 1;  // words 4-5: rank
                 sh->plen = 0;
                 sh->seq = ld_cg_u64(f + 4);         // words 8-9
@@ -727,9 +726,10 @@ struct HeapCta {
                               bool can_serve, unsigned long long rank, unsigned long long seq) {
         Key* par = bat == buf(4) ? buf(1) : buf(4);
         Key* cu = buf(5);
+        uint32_t cur_word = 0;  // leader: exact state word of the held `cur` (0 = unknown)
         if (!served) {
             if (leader()) {
-                lane_claim(target, (1u << kAvail) | (1u << kDelMod));
+                lane_claim(target, (1u << kAvail) | (1u << kDelMod), &cur_word);
                 rec(kEvAcq, target);
             }
             if (can_serve && threadIdx.x < 32) {
@@ -741,7 +741,7 @@ struct HeapCta {
                         st_cg_u64(&hdr->node_count, rank + g);
                         st_cg_u64(&hdr->root_seq, seq + 1 + g);
                         atomicAdd(gate_mine(true), (unsigned long long)g);
-                        root_ticket += g;
+                        sh->root_tk += g;
                         count(cCombined, g);
                         pf_add(pfServed, g);
                         pf_add(pfServeHolds, 1);
@@ -762,6 +762,10 @@ struct HeapCta {
         __syncthreads();
 
         unsigned long long cur = target;  // held
+        if (!(hv.flags & kDbgParkClimb)) {
+            climb_gated(cur, bat, par, cur_word, t3);
+            return;
+        }
         while (cur != 1) {
             const unsigned long long parent = cur >> 1;
             const unsigned long long tc0 = now();
@@ -871,6 +875,143 @@ struct HeapCta {
             }
             cur = parent;
         }
+        if (leader()) lane_unlock(1);
+        pf_add(pfInsRest, now() - t3);
+    }
+
+    // The bottom-up climb (heap.cpp:310-391) under the BU phase gate.  Same
+    // states, transitions and lock order as the reference -- park the slot
+    // (INUSE -> INSHOLD), claim the parent, re-take the slot (INSHOLD ->
+    // INUSE), early stop or merge_step_up, release the slot -- but the gate
+    // guarantees no delete heapify runs during a climb, so nobody else ever
+    // touches a parked slot.  Hence:
+    //   * the park carries no data and is a relaxed red (no release fence);
+    //   * the climber keeps the batch of the node it holds in shared memory
+    //     and re-takes the parked slot with a CAS on the exact word it parked,
+    //     without reloading the keys and without waiting for the CAS before
+    //     merging (its result is checked before any write to the slot);
+    //   * the node it carries up is written once, when it is released;
+    //   * the release fence of each finished slot is paid by another warp.
+    // `cu` holds the held node's batch on entry (the target's, already in
+    // HBM); cur_word is the leader's view of cur's state word (0 if unknown).
+    __device__ void climb_gated(unsigned long long cur, Key* cu, Key* par, uint32_t cur_word,
+                                unsigned long long t3) {
+        constexpr uint32_t kRelLane = T >= 64 ? 32 : 0;
+        auto bidx = [this](const Key* b) { return (int)((b - bufs) / K); };
+        int ci = bidx(cu), pi = bidx(par);
+        const int si = 7;  // staging for the slot's new batch
+        int ni = __ffs(~((1u << ci) | (1u << pi) | (1u << si))) - 1;
+        bool cur_written = true;  // the target's batch is already in HBM
+        while (cur != 1) {
+            const unsigned long long parent = cur >> 1;
+            const unsigned long long tc0 = now();
+            pf_add(pfBuLevels, 1);
+            uint32_t parked = 0;
+            if (leader()) {
+                rec_lane(kEvRel, cur);
+                if (cur_word) {
+                    state_release_relaxed(st(cur), kInUse, kInsHold);
+                    parked = swith(cur_word, kInsHold) + 8u;  // the word the park leaves
+                } else {
+                    state_release(st(cur), kInUse, kInsHold);
+                }
+            }
+            // ---- claim the parent with its keys in flight ----
+            for (;;) {
+                if (leader()) {
+                    if (parent == 1) {
+                        root_lock();
+                        sh->ok[0] = 2;
+                    } else {
+                        uint32_t* pp = st(parent);
+                        Backoff b;
+                        uint32_t w;
+                        for (;;) {
+                            w = state_load(pp);
+                            if (sget(w) == kAvail || sget(w) == kDelMod) break;
+                            { b.pause(); BH_WAIT_NOTE(__LINE__); }
+                        }
+                        sh->cw[0] = w;
+                        sh->ok[0] = 0;
+                    }
+                }
+                __syncthreads();
+                uint32_t ok = 1;
+                if (leader() && sh->ok[0] == 0) {
+                    const uint32_t w = sh->cw[0];
+                    ok = state_cas_relaxed(st(parent), w, swith(w, kInUse));
+                }
+                cta_load<Key, T>(buf(pi), node(parent), K);
+                if (leader() && sh->ok[0] == 0) sh->ok[0] = ok;
+                __syncthreads();
+                if (sh->ok[0]) break;
+            }
+            uint32_t parent_word = 0;
+            if (leader() && parent != 1) {
+                rec(kEvAcq, parent);
+                parent_word = swith(sh->cw[0], kInUse);
+            }
+            const unsigned long long tc1 = now();
+            pf_add(pfBuParent, tc1 - tc0);
+            Key* P = buf(pi);
+            Key* C = buf(ci);
+            // ---- re-take the parked slot (CAS in flight while we merge) ----
+            uint32_t retake_ok = 1;
+            if (leader()) {
+                if (parked) {
+                    retake_ok = state_cas_relaxed(st(cur), parked, swith(parked, kInUse));
+                    cur_word = swith(parked, kInUse);
+                } else {
+                    // word unknown (a combiner claimed the target): poll it
+                    uint32_t* pc = st(cur);
+                    uint32_t w;
+                    Backoff b;
+                    while (sget(w = state_load(pc)) != kInsHold) { b.pause(); BH_WAIT_NOTE(__LINE__); }
+                    retake_ok = state_cas(pc, w, swith(w, kInUse));
+                    cur_word = swith(w, kInUse);
+                }
+                rec(kEvAcq, cur);
+            }
+            pf_add(pfBuRetake, now() - tc1);
+            const bool stop = C[0] >= P[K - 1];
+            bool swap = false;
+            if (stop) {
+                count(cEarlyStops);
+            } else if (elide && !needs_merge_full<Key, K>(C, P)) {
+                count(cElided);
+                swap = true;  // C < P entirely: parent takes C, the slot takes P
+            } else {
+                cta_merge_full<Key, K, T>(C, P, buf(ni), buf(si));
+                count(cMerges);
+            }
+            if (!stop) count(cVisits);
+            __syncthreads();
+            if (leader() && !retake_ok) atomicOr(&hdr->error_flags, (unsigned long long)kErrInteriorEmpty);
+            // the slot's final batch goes to HBM now
+            if (stop) {
+                if (!cur_written) cta_store<Key, T>(node(cur), C, K);
+            } else {
+                cta_store<Key, T>(node(cur), swap ? P : buf(si), K);
+            }
+            __syncthreads();
+            if (threadIdx.x == kRelLane) lane_unlock(cur);
+            if (stop) {
+                if (leader()) lane_unlock(parent);  // parent batch unchanged
+                pf_add(pfInsRest, now() - t3);
+                return;
+            }
+            // carry the parent's new batch up; it is written when released
+            if (!swap) {
+                const int t = ci;
+                ci = ni;
+                ni = t;
+            }
+            cur_written = false;
+            cur = parent;
+            cur_word = parent_word;
+        }
+        cta_store<Key, T>(node(1), buf(ci), K);
+        __syncthreads();
         if (leader()) lane_unlock(1);
         pf_add(pfInsRest, now() - t3);
     }
@@ -1184,6 +1325,9 @@ struct HeapCta {
     __device__ void heapify_down(int ci, unsigned long long t_root, bool pre) {
         constexpr bool kSplit = T >= 64;
         constexpr uint32_t kHalf = kSplit ? T / 2 : T;
+        // upper-half lane with no claim duty (acquire_children polls with its
+        // first two lanes)
+        constexpr uint32_t kRelLane = kSplit ? (T >= 128 ? kHalf + 32 : kHalf + 2) : 0;
         unsigned long long cur = 1;
         uint32_t cur_rel = kAvail;
         const unsigned long long t_start = now();
@@ -1278,7 +1422,10 @@ struct HeapCta {
                 cta_merge_half<Key, K, T, false, true>(cur_s, hdata, node(cur), threadIdx.x, T);
             const unsigned long long tl3 = now();
             __syncthreads();
-            if (leader()) {
+            // The release fence waits for the batch's stores to be acked; a
+            // thread of the upper half (idle until its claim) pays it, so the
+            // lower half starts the carried-batch merge at once.
+            if (threadIdx.x == kRelLane) {
                 lane_unlock(cur, cur_rel);
                 if (lo_locked && !merge_children) lane_unlock(lo, lo_rel);  // unchanged
             }

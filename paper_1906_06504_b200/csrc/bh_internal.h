@@ -31,6 +31,7 @@ constexpr uint32_t kDbgSeqRefill = 0x100;       // reference refill order in eve
 constexpr uint32_t kDbgWriteUnderRoot = 0x200;  // BU target written before the root release
 constexpr uint32_t kDbgSerialLanes = 0x400;     // claim children one after the other
 constexpr uint32_t kDbgNoCombine = 0x800;       // no insert combining in the root queue lock
+constexpr uint32_t kDbgParkClimb = 0x1000;      // reference BU climb (fenced park, reload on re-take)
 
 // Heap header, root-lock guarded (reference heap.hpp:173-177).  One cache
 // line; the partial buffer follows in its own allocation.

@@ -214,6 +214,64 @@ __global__ void __launch_bounds__(T) handoff_bench(uint32_t* node, uint32_t* st,
     if (threadIdx.x == 0) out[me] = (t1 - t0) / iters;
 }
 
+// Latency of loading one 4 KiB node (just written by another SM) into
+// shared memory: VEC bytes per thread (4, 8, 16), NT threads issuing.
+template <int VEC, int NT>
+__global__ void __launch_bounds__(512) nodeload_bench(uint32_t* node, uint32_t* flag, int iters, int other,
+                                                     unsigned long long* out) {
+    __shared__ __align__(16) uint32_t buf[1024];
+    int me;
+    if (blockIdx.x == 0) me = 0;
+    else if ((int)blockIdx.x == other) me = 1;
+    else return;
+    unsigned long long tot = 0;
+    for (int it = 0; it < iters; ++it) {
+        if (me == 1) {
+            // writer: rewrite the node, publish
+            for (int i = threadIdx.x; i < 256; i += 512) __stcg(reinterpret_cast<uint4*>(node) + i, make_uint4(it, it, it, it));
+            __syncthreads();
+            if (threadIdx.x == 0) { __threadfence(); atomicExch(flag, (uint32_t)(2 * it + 1)); }
+            if (threadIdx.x == 0) while (state_load(flag) != (uint32_t)(2 * it + 2)) {}
+            __syncthreads();
+        } else {
+            if (threadIdx.x == 0) while (state_load(flag) != (uint32_t)(2 * it + 1)) {}
+            __syncthreads();
+            unsigned long long t0 = clock64();
+            if (threadIdx.x < NT) {
+                if constexpr (VEC == 16) {
+                    for (int i = threadIdx.x; i < 256; i += NT) reinterpret_cast<uint4*>(buf)[i] = __ldcg(reinterpret_cast<const uint4*>(node) + i);
+                } else if constexpr (VEC == 8) {
+                    for (int i = threadIdx.x; i < 512; i += NT) reinterpret_cast<uint2*>(buf)[i] = __ldcg(reinterpret_cast<const uint2*>(node) + i);
+                } else {
+                    for (int i = threadIdx.x; i < 1024; i += NT) buf[i] = __ldcg(node + i);
+                }
+            }
+            __syncthreads();
+            unsigned long long t1 = clock64();
+            tot += t1 - t0;
+            if (threadIdx.x == 0) { if (buf[5] != (uint32_t)it) tot += 1000000000ull; atomicExch(flag, (uint32_t)(2 * it + 2)); }
+            __syncthreads();
+        }
+    }
+    if (me == 0 && threadIdx.x == 0) out[0] = tot / iters;
+}
+
+template <int VEC, int NT>
+void run_nodeload(const char* name) {
+    uint32_t *node, *flag;
+    unsigned long long* o;
+    CK(cudaMalloc(&node, 4096));
+    CK(cudaMalloc(&flag, 256));
+    CK(cudaMemset(flag, 0, 256));
+    CK(cudaMalloc(&o, 16));
+    nodeload_bench<VEC, NT><<<148, 512>>>(node, flag, 2000, 74, o);
+    CK(cudaDeviceSynchronize());
+    unsigned long long c;
+    CK(cudaMemcpy(&c, o, 8, cudaMemcpyDeviceToHost));
+    printf("nodeload %-12s vec=%2d threads=%3d : %llu cycles\n", name, VEC, NT, c);
+    cudaFree(node); cudaFree(flag); cudaFree(o);
+}
+
 // Round trip of one atomicCAS / red+poll from a single thread.
 __global__ void atom_rt(uint32_t* p, int iters, unsigned long long* out) {
     unsigned long long t0 = clock64();
@@ -375,6 +433,18 @@ int main(int argc, char** argv) {
             run_half<1024, 512, 8, 1>("quaternary");
             run_half<1024, 512, 1, 1>("quaternary");
             run_half<1024, 256, 4, 1>("quaternary");
+        }
+        if (w == "load") {
+            run_nodeload<16, 256>("remote-written");
+            run_nodeload<16, 512>("remote-written");
+            run_nodeload<16, 128>("remote-written");
+            run_nodeload<8, 512>("remote-written");
+            run_nodeload<4, 512>("remote-written");
+            run_handoff<1 | 2 | 8>(74, "full (ld.acq polls)");
+            run_handoff<2 | 8>(74, "store only");
+            run_handoff<1 | 8>(74, "load only");
+            run_handoff<8>(74, "state only, CAS");
+            run_handoff<0>(74, "state only, store");
         }
         if (w == "m0") run_merge<1024, 512, 0>("full (current)");
         if (w == "m8") run_merge<1024, 512, 8>("quaternary E8 vec full");
