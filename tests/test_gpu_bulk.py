@@ -115,7 +115,7 @@ def mixed_ops(rng, n_ops, k, partial_pct, key_hi, pre_nodes=0):
 
 
 @pytest.mark.parametrize("variant", [Variant.TD, Variant.BU])
-@pytest.mark.parametrize("k", [1, 4, 16, 64, 1024])
+@pytest.mark.parametrize("k", [1, 4, 16, 64, 128, 256, 1024, 2048])
 def test_mixed_concurrent_multiset_and_invariants(variant, k):
     """SPEC acceptance 1 analogue: 50/50 ins/del, 20% partial batches, many
     CTAs at once; quiescent properties 1-3 and multiset conservation."""

@@ -15,11 +15,105 @@
 #include <string>
 
 #include "../../paper_1906_06504_b200/csrc/bh_device.cuh"
-#include "../../paper_1906_06504_b200/csrc/bh_select.cuh"
+#include "mb_variants.cuh"
 
 using namespace bh;
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1);} } while (0)
+
+// Padded layout: element i lives at i + i/32 (one pad word per 32), so
+// split-search probes at power-of-two strides fall in different banks.
+__device__ __forceinline__ uint32_t padi(uint32_t i) { return i + (i >> 5); }
+
+template <typename Key, int K, int P>
+__device__ __forceinline__ void half_pad(const Key* A, const Key* B, Key* out) {
+    const uint32_t t0 = threadIdx.x * P;
+    if (t0 >= (uint32_t)K) return;
+    const uint32_t d = t0;
+    const uint32_t lo = 0, hi = d < K ? d : K;
+    uint32_t base = lo;
+#pragma unroll
+    for (uint32_t step = (uint32_t)K; step > 0; step >>= 1) {
+        const uint32_t p = base + step;
+        if (p <= hi && A[padi(p - 1)] <= B[padi(d - p)]) base = p;
+    }
+    const uint32_t i = base, j = d - base;
+    Key a[P + 1], b[P + 1];
+#pragma unroll
+    for (int e = 0; e < P; ++e) {
+        a[e] = i + e < K ? A[padi(i + e)] : KeyLimits<Key>::kMax;
+        b[e] = j + e < K ? B[padi(j + e)] : KeyLimits<Key>::kMax;
+    }
+    a[P] = b[P] = KeyLimits<Key>::kMax;
+    uint32_t ra = K - i, rb = K - j;
+    Key o[P];
+#pragma unroll
+    for (int e = 0; e < P; ++e) {
+        const bool ta = rb == 0 || (ra != 0 && a[0] <= b[0]);
+        o[e] = ta ? a[0] : b[0];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            a[q] = ta ? a[q + 1] : a[q];
+            b[q] = ta ? b[q] : b[q + 1];
+        }
+        ra -= ta;
+        rb -= !ta;
+    }
+#pragma unroll
+    for (int e = 0; e < P; ++e) out[padi(t0 + e)] = o[e];
+}
+
+template <typename Key, int K, int T, int P>
+__global__ void __launch_bounds__(T) halfpad_bench(const Key* in, int iters, unsigned long long* out, Key* sink) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    constexpr int KP = K + K / 32;
+    Key* A = reinterpret_cast<Key*>(sm);
+    Key* B = A + KP;
+    Key* H = B + KP;
+    for (int i = threadIdx.x; i < K; i += T) { A[padi(i)] = in[i]; B[padi(i)] = in[K + i]; }
+    __syncthreads();
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        half_pad<Key, K, P>(A, B, H);
+        __syncthreads();
+        if (threadIdx.x == 0) A[0] = H[0] < A[0] ? H[0] : A[0];
+        __syncthreads();
+    }
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) out[0] = (t1 - t0) / iters;
+    for (int i = threadIdx.x; i < K; i += T) sink[i] = H[padi(i)];
+}
+
+template <int K, int T, int P>
+void run_halfpad(const char* name) {
+    using Key = uint32_t;
+    std::mt19937 rng(1);
+    std::vector<Key> h(2 * K);
+    for (auto& x : h) x = rng() >> 1;
+    std::sort(h.begin(), h.begin() + K);
+    std::sort(h.begin() + K, h.end());
+    Key *d, *sink;
+    unsigned long long* o;
+    CK(cudaMalloc(&d, 2 * K * 4));
+    CK(cudaMalloc(&sink, 2 * K * 4 + 16));
+    CK(cudaMalloc(&o, 8 * 8));
+    CK(cudaMemcpy(d, h.data(), 2 * K * 4, cudaMemcpyHostToDevice));
+    auto kern = halfpad_bench<Key, K, T, P>;
+    const int smem = 3 * (K + K / 32) * 4 + 64;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<1, T, smem>>>(d, 1, o, sink);
+    CK(cudaDeviceSynchronize());
+    std::vector<Key> got(K), ref(2 * K);
+    CK(cudaMemcpy(got.data(), sink, K * 4, cudaMemcpyDeviceToHost));
+    std::merge(h.begin(), h.begin() + K, h.begin() + K, h.end(), ref.begin());
+    if (!std::equal(got.begin(), got.end(), ref.begin())) printf("halfpad %s WRONG OUTPUT\n", name);
+    kern<<<1, T, smem>>>(d, 2000, o, sink);
+    CK(cudaDeviceSynchronize());
+    unsigned long long c;
+    CK(cudaMemcpy(&c, o, 8, cudaMemcpyDeviceToHost));
+    printf("halfpad %-20s K=%d T=%d P=%d : %llu cycles\n", name, K, T, P, c);
+    cudaFree(d); cudaFree(sink); cudaFree(o);
+}
 
 // Half-merge variants: P outputs per thread, binary (Q=0) or quaternary (Q=1)
 // split search.
@@ -424,6 +518,13 @@ void run_handoff(int other, const char* name) {
 int main(int argc, char** argv) {
     if (argc > 1) {
         std::string w = argv[1];
+        if (w == "pad") {
+            run_half<1024, 512, 4, 0>("binary");
+            run_halfpad<1024, 512, 4>("padded binary");
+            run_halfpad<1024, 512, 2>("padded binary");
+            run_halfpad<1024, 512, 8>("padded binary");
+            run_halfpad<1024, 256, 4>("padded binary");
+        }
         if (w == "half") {
             run_half<1024, 512, 4, 0>("binary");
             run_half<1024, 512, 4, 1>("quaternary");
