@@ -356,6 +356,42 @@ struct HeapCta {
     __device__ __forceinline__ unsigned long long* gate_other(bool climb) {
         return climb ? &hdr->deleters : &hdr->climbers;
     }
+    // Phase token (root-lock guarded).  Ops of the open phase enter until an
+    // op of the other kind arrives and closes it; that op (and its kind)
+    // wait outside the root queue until the running kind has drained, then
+    // the first of them flips the phase and its whole batch enters.  Leader
+    // lane, root held.  Returns true when the op may start (counted).
+    __device__ bool gate_try(bool climb) {
+        const unsigned long long me = climb ? 0ull : 1ull;
+        const unsigned long long ph = ld_cg_u64(&hdr->gate_phase);
+        const unsigned long long closing = ld_cg_u64(&hdr->gate_closing);
+        const unsigned long long other = ld_cg_u64(gate_other(climb));
+        if (ph == me && !closing) {
+            atomicAdd(gate_mine(climb), 1ull);  // ordered before the root release
+            return true;
+        }
+        if (ph != me && other == 0) {
+            st_cg_u64(&hdr->gate_phase, me);
+            st_cg_u64(&hdr->gate_closing, 0ull);
+            atomicAdd(gate_mine(climb), 1ull);
+            return true;
+        }
+        if (ph != me) st_cg_u64(&hdr->gate_closing, 1ull);
+        return false;
+    }
+    // Wait (root not held, not queued) until a retry can succeed or can
+    // close the running phase.
+    __device__ void gate_wait(bool climb) {
+        const unsigned long long me = climb ? 0ull : 1ull;
+        Backoff b;
+        for (;;) {
+            const unsigned long long ph = __ldcg(&hdr->gate_phase);
+            const unsigned long long closing = __ldcg(&hdr->gate_closing);
+            const unsigned long long other = __ldcg(gate_other(climb));
+            if (ph == me ? !closing : (other == 0 || !closing)) return;
+            { b.pause(); BH_WAIT_NOTE(__LINE__); }
+        }
+    }
     __device__ void gate_leave(bool climb) {
         __threadfence();
         atomicAdd(gate_mine(climb), ~0ull);  // -1, after every write of the op
@@ -437,7 +473,6 @@ struct HeapCta {
         // ---- root phase (heap.cpp:126-167) ----
         if (leader()) {
             uint32_t gated = 0;
-            Backoff gb;
             const bool combinable =
                 hv.variant == BH_BU && n == (uint32_t)K && (hv.flags & kDbgNoCombine) == 0;
             bool served = false;
@@ -447,7 +482,6 @@ struct HeapCta {
                 const unsigned long long nd = ld_cg_u64(&hdr->node_count);
                 const unsigned long long pl = ld_cg_u64(&hdr->partial_len);
                 const unsigned long long sq = ld_cg_u64(&hdr->root_seq);
-                const unsigned long long dl = hv.variant == BH_BU ? ld_cg_u64(gate_other(true)) : 0;
                 sh->nodes = nd;
                 sh->plen = pl;
                 sh->seq = sq;
@@ -455,13 +489,12 @@ struct HeapCta {
                 const bool climbs = hv.variant == BH_BU && n + (uint32_t)pl >= (uint32_t)K && nd >= 1 &&
                                     nd < hv.max_nodes;
                 if (!climbs) break;
-                if (dl == 0) {
-                    atomicAdd(gate_mine(true), 1ull);  // ordered before the root release
+                if (gate_try(true)) {
                     gated = 1;
                     break;
                 }
                 root_unlock(false);
-                { gb.pause(); BH_WAIT_NOTE(__LINE__); }
+                gate_wait(true);
             }
             if (served) {
                 // a combiner ran the root phase: rank, claimed target, sequence
@@ -1168,19 +1201,16 @@ struct HeapCta {
             if (hv.variant == BH_BU) {
                 // BU phase gate: a delete that will heapify (>= 2 nodes) waits
                 // until no bottom-up climb is in flight
-                Backoff gb;
                 for (;;) {
                     root_lock(false);
                     const unsigned long long nodes_now = ld_cg_u64(&hdr->node_count);
-                    const unsigned long long climbers = ld_cg_u64(gate_other(false));
                     if (nodes_now < 2) break;
-                    if (climbers == 0) {
-                        atomicAdd(gate_mine(false), 1ull);
+                    if (gate_try(false)) {
                         gated = 1;
                         break;
                     }
                     root_unlock(false);
-                    { gb.pause(); BH_WAIT_NOTE(__LINE__); }
+                    gate_wait(false);
                 }
                 rec(kEvAcq, 1);
             } else {

@@ -48,7 +48,9 @@ struct alignas(128) Header {
     unsigned long long root_tail;     // root queue-lock ticket dispenser
     unsigned long long climbers;      // BU: in-flight bottom-up climbs
     unsigned long long deleters;      // BU: in-flight delete heapifies
-    unsigned long long pad1[13];
+    unsigned long long gate_phase;    // BU: kind that may start (0 climbs, 1 heapifies); root-lock guarded
+    unsigned long long gate_closing;  // BU: an op of the other kind waits for the phase
+    unsigned long long pad1[11];
 };
 
 // Device counters (reference HeapCounters, heap.hpp:49-58).
