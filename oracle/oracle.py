@@ -322,6 +322,22 @@ def ref_knapsack_bb_subprocess(kind: int, n: int, rng_range: int, seed: int, wor
     return {"best": int(best), "explored": int(explored), "gc": int(gc), "seconds": float(secs)}
 
 
+REF_HISTCHECK = os.path.join(HERE, "_ref", "ref_histcheck")
+
+
+def ref_history_check(text: str, variant: int, k: int) -> dict:
+    """The reference's History::parse + check_td/check_bu (+ overlap windows
+    for BU, + check_exhaustive for <= 16 ops) on a history in its text
+    format, via oracle/_ref/ref_histcheck (a separate process)."""
+    import subprocess
+    r = subprocess.run([REF_HISTCHECK, str(variant), str(k)], input=text, capture_output=True, text=True,
+                       timeout=600)
+    if r.returncode != 0:
+        return {"error": r.stderr.strip()}
+    p, o, e, n = (int(x) for x in r.stdout.split())
+    return {"pass": bool(p), "overlap_ok": bool(o), "exhaustive": e, "ops": n, "detail": r.stderr.strip()}
+
+
 class RefHeap:
     """The reference GeneralizedHeap behind ctypes (for cross-checks)."""
 

@@ -90,3 +90,28 @@ def test_split_schedule_widths_mixed_td(k):
                               for i, o in enumerate(ops) if o["kind"] == 1] + [np.zeros(0, np.uint64)])
     acc = np.sort(np.concatenate([deleted.astype(np.uint64), heap.collect_resident()]))
     assert np.array_equal(acc, O.sort_u64(pool))
+
+
+@pytest.mark.skipif(not __import__("os").path.exists(O.REF_HISTCHECK), reason="reference checker not built")
+@pytest.mark.parametrize("variant", [Variant.TD, Variant.BU])
+@pytest.mark.parametrize("key_hi", [12, 1 << 40])
+def test_device_history_passes_reference_checker(variant, key_hi):
+    """A recorded concurrent device run, written in the reference's history
+    text format by paper_1906_06504_b200.history, is accepted by the
+    reference's own History::parse and check_td / check_bu (and, for BU, its
+    overlap-window scan); small histories also by check_exhaustive."""
+    from paper_1906_06504_b200.history import History, history_of
+    for trial in range(4):
+        rng = np.random.default_rng(500 + trial + int(variant) * 10 + (key_hi & 7))
+        k = 2 if key_hi == 12 else 8
+        n_ops = 14 if trial == 0 else 400
+        ops, pool, out_len, _ = mixed_ops(rng, n_ops, k, 25, key_hi)
+        heap = GeneralizedHeap(variant, k, n_ops + 8, record=True)
+        r = heap.run_ops(ops, pool, out_len, ctas=64)
+        h = history_of(heap, ops, r, pool)
+        text = h.serialize()
+        assert History.parse(text, int(variant), k).serialize() == text
+        res = O.ref_history_check(text, int(variant), k)
+        assert res.get("pass") and res["overlap_ok"], res
+        if len(h.ops) <= 16:
+            assert res["exhaustive"] == 1, res
