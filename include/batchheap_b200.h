@@ -278,6 +278,15 @@ typedef struct {
 BH_API int bh_knapsack_bb(uint32_t n, const uint32_t* weight, const uint32_t* benefit, uint64_t capacity,
                           const bh_bb_cfg* cfg, int device, bh_bb_outcome* out);
 
+/* plan_batches (proj/src/bench.cpp:21-47): the batch lengths the reference's
+ * benchmark inserts for n_keys keys split over `workers` contiguous shares
+ * (full_batch_pct % full k-batches, the rest 1..k-1 keys, mt19937_64 per
+ * worker).  Writes up to cap lengths (and each batch's worker) in worker
+ * order; *n_out = number of batches.  Pass lens = NULL to size. */
+BH_API int bh_plan_batches(uint32_t k, uint64_t n_keys, uint32_t workers, uint32_t full_batch_pct,
+                           uint64_t seed, uint32_t* lens, uint32_t* worker_of, uint64_t cap,
+                           uint64_t* n_out);
+
 /* Library build identity (sm arch, compile flags). */
 BH_API const char* bh_build_info(void);
 

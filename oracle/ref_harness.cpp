@@ -186,7 +186,8 @@ int ref_phase(int variant, std::uint32_t k, std::uint64_t n_keys, std::uint32_t 
 
 // Reference's own sweep row (proj/src/bench.cpp:163-185): correctness pass
 // then timed pass; out[0]=wall s, out[1]=ops, out[2]=merges,
-// out[3]=early_stops, out[4]=mean_nodes_traversed.
+// out[3]=early_stops, out[4]=mean_nodes_traversed, out[5]=inserts,
+// out[6]=deletes (out must hold 7 doubles).
 int ref_run_workload(int variant, std::uint32_t k, std::uint32_t workers, std::uint64_t total_keys,
                      int order, int pattern, std::uint32_t initial_levels,
                      std::uint32_t full_pct, std::uint64_t seed, double* out) {
@@ -207,6 +208,8 @@ int ref_run_workload(int variant, std::uint32_t k, std::uint32_t workers, std::u
         out[2] = static_cast<double>(row.counters.merges);
         out[3] = static_cast<double>(row.counters.early_stops);
         out[4] = row.mean_nodes_traversed;
+        out[5] = static_cast<double>(row.counters.inserts);
+        out[6] = static_cast<double>(row.counters.deletes);
     });
 }
 

@@ -98,6 +98,7 @@ SIGNATURES = {
     "bh_bit_reverse": (_u64, [_u64, C.c_uint]),
     "bh_generate_keys": (_i, [_i, _u64, _u64, _u32, _vp]),
     "bh_build_info": (C.c_char_p, []),
+    "bh_plan_batches": (_i, [_u32, _u64, _u32, _u32, _u64, _vp, _vp, _u64, C.POINTER(_u64)]),
     "bh_grid_graph_edges": (_u64, [_u32, _u32]),
     "bh_grid_graph": (_i, [_u32, _u32, _u64, _vp, _vp, _vp]),
     "bh_sssp": (_i, [_u32, _vp, _vp, _vp, _u32, C.POINTER(bh_sssp_cfg), _i, _vp, C.POINTER(bh_sssp_stats)]),

@@ -793,6 +793,35 @@ int bh_merge_split(uint32_t key_bits, uint32_t k, const void* a, const void* b, 
     return rc == BH_OK ? rc : fail(rc, "merge launch failed");
 }
 
+int bh_plan_batches(uint32_t k, uint64_t n_keys, uint32_t workers, uint32_t full_batch_pct, uint64_t seed,
+                    uint32_t* lens, uint32_t* worker_of, uint64_t cap, uint64_t* n_out) {
+    // plan_batches (proj/src/bench.cpp:21-47): each worker's contiguous share
+    // of the keys, chopped into k-batches, a (100 - full_batch_pct)% share of
+    // them shortened to a random 1..k-1 keys.
+    if (!n_out || k == 0 || workers == 0) return fail(BH_E_CONFIG, "bad batch plan arguments");
+    const uint64_t share = n_keys / workers;
+    uint64_t begin = 0, count = 0;
+    for (uint32_t w = 0; w < workers; ++w) {
+        const uint64_t end = (w + 1 == workers) ? n_keys : begin + share;
+        std::mt19937_64 rng(seed ^ (0xb5297a4d3f512d6bull + w));
+        std::uniform_int_distribution<int> pct(0, 99);
+        std::uniform_int_distribution<std::size_t> part(1, k > 1 ? k - 1 : 1);
+        uint64_t at = begin;
+        while (at < end) {
+            std::size_t len = k;
+            if (k > 1 && pct(rng) >= static_cast<int>(full_batch_pct)) len = part(rng);
+            len = std::min<uint64_t>(len, end - at);
+            if (lens && count < cap) lens[count] = (uint32_t)len;
+            if (worker_of && count < cap) worker_of[count] = w;
+            ++count;
+            at += len;
+        }
+        begin = end;
+    }
+    *n_out = count;
+    return BH_OK;
+}
+
 int bh_generate_keys(int order, uint64_t n, uint64_t seed, uint32_t key_bits, void* out) {
     if (!out && n) return fail(BH_E_CONFIG, "null output");
     if (key_bits != 32 && key_bits != 64) return fail(BH_E_CONFIG, "key_bits must be 32 or 64");

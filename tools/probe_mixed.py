@@ -63,7 +63,7 @@ for v in a.variants.split(","):
         heap.close()
 if a.ref:
     from oracle import oracle as O
-    out = np.zeros(5, np.float64)
+    out = np.zeros(7, np.float64)
     w = os.cpu_count()
     for v in a.variants.split(","):
         st = O.ref().ref_run_workload(1 if v == "bu" else 0, k, w, n, 0, 1, a.levels, 100, 1, out)
