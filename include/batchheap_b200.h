@@ -32,7 +32,9 @@ extern "C" {
  *   BH_E_INVALID_KEY  <- std::invalid_argument "key reaches sentinel" (proj/src/batch.cpp:13-15)
  *   BH_E_CUDA         -- device/runtime failure (no reference analogue)
  *   BH_E_INTERNAL     -- protocol invariant broken (reference std::logic_error,
- *                        proj/src/heap.cpp:462-463)                              */
+ *                        proj/src/heap.cpp:462-463); the synchronous entry
+ *                        points (bh_insert, bh_delete_min, bh_run_ops) check
+ *                        the device fault flags after every call             */
 enum {
     BH_OK = 0,
     BH_E_CONFIG = 1,

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -239,6 +240,23 @@ void put_ctx(bh_heap* h, OpCtx* c) {
 }
 
 // One operation through its own context (bh_insert / bh_delete_min).
+// Device-detected protocol faults (reference: the std::logic_error
+// "sentinel escaped" of heap.cpp:462-463 and asserts) after a synchronous
+// call: BH_E_INTERNAL with the flags named.
+int check_device_faults(bh_heap* h) {
+    unsigned long long flags = 0;
+    cudaError_t e = cudaMemcpy(&flags, reinterpret_cast<const char*>(h->d_hdr) + offsetof(Header, error_flags),
+                               sizeof(flags), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "error flags");
+    if (!flags) return BH_OK;
+    std::string msg = "device protocol fault:";
+    if (flags & kErrSentinelEscaped) msg += " sentinel escaped (heap.cpp:462-463);";
+    if (flags & kErrInteriorEmpty) msg += " interior node empty;";
+    if (flags & kErrEventOverflow) msg += " event log overflow;";
+    if (flags & kErrRetake) msg += " parked slot taken during a gated climb;";
+    return fail(BH_E_INTERNAL, msg);
+}
+
 int single_op(bh_heap* h, const bh_op& op, const void* keys, uint32_t n, void* out, uint32_t* n_out) {
     if (h->flags & BH_FLAG_RECORD)
         return fail(BH_E_CONFIG, "single-op calls are not recorded; use bh_run_ops on RECORD handles");
@@ -285,6 +303,8 @@ int single_op(bh_heap* h, const bh_op& op, const void* keys, uint32_t n, void* o
     if (out && st == BH_OK) std::memcpy(out, c->h + lay.out, (size_t)len * h->key_size);
     if (n_out) *n_out = st == BH_OK ? len : 0;
     put_ctx(h, c);
+    const int faults = check_device_faults(h);
+    if (faults != BH_OK) return faults;
     switch (st) {
         case BH_OK:
             return BH_OK;
@@ -529,7 +549,7 @@ int bh_run_ops(bh_heap* h, const bh_op* ops, uint64_t n_ops, const void* key_poo
     if (out_lens) BH_CUDA(cudaMemcpyAsync(out_lens, d_lens, n_ops * 4, cudaMemcpyDeviceToHost, s));
     if (out_seq) BH_CUDA(cudaMemcpyAsync(out_seq, d_seq, n_ops * 8, cudaMemcpyDeviceToHost, s));
     BH_CUDA(cudaStreamSynchronize(s));
-    return BH_OK;
+    return check_device_faults(h);
 }
 
 int bh_plan_phase(bh_heap* h, int kind, uint64_t n_keys, bh_op* ops, int on_device, void* stream) {

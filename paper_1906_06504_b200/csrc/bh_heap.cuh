@@ -1019,7 +1019,7 @@ struct HeapCta {
             }
             if (!stop) count(cVisits);
             __syncthreads();
-            if (leader() && !retake_ok) atomicOr(&hdr->error_flags, (unsigned long long)kErrInteriorEmpty);
+            if (leader() && !retake_ok) atomicOr(&hdr->error_flags, (unsigned long long)kErrRetake);
             // the slot's final batch goes to HBM now
             if (stop) {
                 if (!cur_written) cta_store<Key, T>(node(cur), C, K);

@@ -71,6 +71,7 @@ enum ErrorFlag : unsigned long long {
     kErrSentinelEscaped = 1ull << 0,  // heap.cpp:462-463
     kErrInteriorEmpty = 1ull << 1,    // heap.cpp:286 assert
     kErrEventOverflow = 1ull << 2,
+    kErrRetake = 1ull << 3,           // gated BU climb: re-take CAS of the parked slot failed
 };
 
 enum EventKind : uint16_t { kEvInv = 0, kEvRes = 1, kEvAcq = 2, kEvRel = 3 };
