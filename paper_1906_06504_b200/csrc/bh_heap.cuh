@@ -90,6 +90,8 @@ enum ProfIdx {
     pfBuParent, // BU climb: park -> parent claimed (cycles)
     pfBuRetake, // BU climb: re-take of the parked slot (cycles)
     pfBuLevels, // BU climb levels
+    pfSplitA,   // delete root split: refill half done (cycles from split start)
+    pfSplitB,   // delete root split: children half done
     kNumProf
 };
 
@@ -1303,10 +1305,13 @@ struct HeapCta {
         const bool split = T >= 64 && nodes >= 4;
         if (split) {
             constexpr uint32_t kHalf = T / 2;
-            if (threadIdx.x < kHalf)
+            if (threadIdx.x < kHalf) {
                 refill_last(last, cur_s, 0, kHalf, 1);
-            else
+                pf_add(pfSplitA, now() - ta);
+            } else {
                 acquire_children(1, buf(1), buf(2), kHalf, kHalf, 2);
+                if (prof && threadIdx.x == kHalf) atomicAdd(&hv.prof[pfSplitB], now() - ta);
+            }
             __syncthreads();
         } else {
             refill_last(last, cur_s, 0, T, 0);

@@ -278,7 +278,7 @@ class GeneralizedHeap:
                       "del_ops", "del_root_wait", "del_root_hold", "del_rest", "child_wait",
                       "levels", "cta_cycles", "rs_head", "rs_child", "rs_last", "rs_load",
                       "rs_fill", "lv_acq", "lv_load", "lv_merge", "lv_rel", "served",
-                      "serve_holds", "bu_parent", "bu_retake", "bu_levels")
+                      "serve_holds", "bu_parent", "bu_retake", "bu_levels", "split_a", "split_b")
 
     def profile(self, reset: bool = True) -> dict:
         """SM-cycle profile of a BH_FLAG_PROFILE heap (see bh_profile)."""

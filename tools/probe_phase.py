@@ -68,4 +68,5 @@ for k in a.k:
                 bl = max(p['bu_levels'], 1)
                 print(f"   insert combining: served {p['served']} in {p['serve_holds']} holds | climb levels/ins {p['bu_levels']/max(p['ins_ops'],1):.2f} "
                       f"parent-claim us {us(p['bu_parent'], bl):.2f} retake us {us(p['bu_retake'], bl):.2f}", flush=True)
+                print(f"   delete root split: refill half {us(p['split_a'], d):.2f} us, children half {us(p['split_b'], d):.2f} us", flush=True)
             heap.close()
