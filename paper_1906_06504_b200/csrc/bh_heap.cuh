@@ -12,32 +12,32 @@
 //   do_delete   heap.cpp:420-465   root take, refill (:467-531), partial
 //                                  re-merge (:533-545), heapify (:547-667)
 //
-// The throughput of a lock-based heap is set by how long each op holds the
-// root (and, for deletes, each level): a chain of dependent L2/HBM round
-// trips, not bandwidth.  B200-specific choices that shorten the chain (none
-// changes the protocol's states, transitions or lock order):
-//   * node state words carry a version (bh_device.cuh): a node's keys are
-//     loaded in the same round trip as the CAS that claims it, and the load
-//     is kept only if the claim succeeds;
-//   * a node's two children are claimed by two lanes at once;
-//   * the next level's children (and the delete's refill node) are
-//     prefetched into L2 while the current level merges;
-//   * the delete's refill claims children 2 and 3 before the last node
-//     (ancestor-first, as every walk) and releases the last node together
-//     with the first heapify level;
-//   * the carried batch stays in shared memory and is written back once, when
-//     its lock is released; the BU target is written after the root release
-//     (the target is already INUSE);
-//   * the root is a FIFO array queue lock (one flag line per waiter);
-//   * locks are released by one red.release.gpu after a CTA barrier (the
-//     barrier orders every thread's stores before the release);
-//   * counters are per-CTA registers folded into global memory at exit.
+// The throughput of a lock-based heap is set by chains of dependent lock
+// hand-offs and merges, not by bandwidth.  Choices that
+// shorten the chains (none changes the protocol's states, transitions, lock
+// order or the released node contents):
+//   * versioned state words (bh_device.cuh): a node's keys load in the same
+//     round trip as the relaxed CAS that claims it (the acquire is the poll
+//     that saw the release); both children are claimed by two lanes at once;
+//   * the root is a FIFO array queue lock whose holder, when it is a BU
+//     full-batch insert, also runs the root phase of the BU full-batch
+//     inserts queued behind it (serve_inserts: insert combining);
+//   * heapify_down's two-phase level schedule: the node is released right
+//     after the first-half merges that decide its batch; the carried and lo
+//     batches are finished afterwards while the other half of the CTA claims
+//     the next level and precomputes its H; the root's refill and children
+//     claim run side by side;
+//   * the gated BU climb (climb_gated): no fence on the park, no reload on
+//     the re-take, the carried batch written once;
+//   * release fences are paid by a lane whose warp has nothing else to do;
+//     the next level's nodes and the next deletes' refill nodes are
+//     prefetched into L2; counters are per-CTA registers folded at exit.
 //
 // Deliberate deviations from the reference, each fixing a reference bug:
 //   * heapify's merge elision places the batch holding the smaller keys in
 //     the hi child on an equal-maxima tie (heap.cpp:628-636);
 //   * BU heaps run a phase gate: a bottom-up climb and a delete heapify
-//     never overlap (see gate_* below).
+//     never overlap (a phase token, see gate_* below).
 #pragma once
 
 #include "bh_device.cuh"
