@@ -169,8 +169,9 @@ def run_reference_arm(a, rank: int, world: int):
     # bounded sample: the full configs[1] workload when it fits in a few
     # seconds per step on this host, else 2^24 keys (same K, same generator)
     log2n = a.log2n
-    t_probe = sum(cpu_reference(20, a.k, a.variant, threads))
-    projected = t_probe * (1 << (log2n - 20)) * 1.4
+    probe = min(20, log2n)
+    t_probe = sum(cpu_reference(probe, a.k, a.variant, threads))
+    projected = t_probe * (1 << (log2n - probe)) * 1.4
     if projected * (a.steps + a.warmup) > 240:
         log2n = min(log2n, 24)
     n = 1 << log2n
