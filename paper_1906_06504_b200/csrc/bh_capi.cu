@@ -114,6 +114,7 @@ struct bh_heap {
     uint32_t* d_root_flags = nullptr;
     Header* d_hdr = nullptr;
     void* d_partial = nullptr;
+    void* d_mailbox = nullptr;  // BU: carried batches handed to served deletes
     unsigned long long* d_counters = nullptr;
     unsigned long long* d_prof = nullptr;
     unsigned long long* d_tickets = nullptr;  // ring of bulk tickets
@@ -147,6 +148,7 @@ struct bh_heap {
         v.root_flags = d_root_flags;
         v.hdr = d_hdr;
         v.partial = d_partial;
+        v.mailbox = d_mailbox;
         v.counters = d_counters;
         v.prof = d_prof;
         v.slot_count = slot_count;
@@ -391,6 +393,9 @@ int bh_create(bh_heap** out, int variant, uint32_t k, uint32_t max_nodes, uint32
     if ((e = cudaMalloc(&h->d_hdr, sizeof(Header))) != cudaSuccess) return cleanup(cuda_fail(e, "hdr"));
     if ((e = cudaMalloc(&h->d_partial, std::max<size_t>((size_t)k * h->key_size, 16))) != cudaSuccess)
         return cleanup(cuda_fail(e, "partial"));
+    if (variant == BH_BU &&
+        (e = cudaMalloc(&h->d_mailbox, (size_t)kRootQueue * k * h->key_size)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "mailbox"));
     if ((e = cudaMalloc(&h->d_counters, kNumCounters * 8)) != cudaSuccess)
         return cleanup(cuda_fail(e, "counters"));
     if ((e = cudaMalloc(&h->d_tickets, kTicketRing * 128)) != cudaSuccess)
@@ -441,6 +446,7 @@ void bh_destroy(bh_heap* h) {
     cudaFree(h->d_root_flags);
     cudaFree(h->d_hdr);
     cudaFree(h->d_partial);
+    cudaFree(h->d_mailbox);
     cudaFree(h->d_counters);
     cudaFree(h->d_prof);
     cudaFree(h->d_tickets);

@@ -34,6 +34,17 @@ __device__ __forceinline__ uint32_t state_load(const uint32_t* p) {
     return v;
 }
 
+// Polling load without acquire semantics: ld.acquire.gpu invalidates the
+// SM's L1 (CCTL.IVALL) on every poll, which stalls the shared-memory work
+// of the other warps on the SM.  Spin with this, then acquire_fence() once
+// the awaited word is seen (relaxed load + fence = acquire pattern).
+__device__ __forceinline__ uint32_t state_poll(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void acquire_fence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ bool state_cas(uint32_t* p, uint32_t expected, uint32_t desired) {
     uint32_t old;
     asm volatile("atom.acq_rel.gpu.global.cas.b32 %0, [%1], %2, %3;"
@@ -58,6 +69,12 @@ __device__ __forceinline__ bool state_cas_relaxed(uint32_t* p, uint32_t expected
 
 __device__ __forceinline__ void state_store_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// A strong store with no ordering of its own: publishes data only when a
+// release fence (e.g. an earlier state_release by the same thread) has
+// already ordered the CTA's writes before it.
+__device__ __forceinline__ void state_store_relaxed(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Node state words carry a version above the 3-bit state: word = ver<<3 |
@@ -157,6 +174,29 @@ struct Backoff {
         if (n > 32) __nanosleep(n > 64 ? 256 : 64);
     }
 };
+// For a waiter whose wake-up is on a critical path (a delete that a delete
+// server may hand a continuation): short sleeps only.
+struct QuickBackoff {
+    uint32_t n = 0;
+    __device__ __forceinline__ void pause() {
+        ++n;
+        if (n > 32) __nanosleep(32);
+    }
+};
+
+// Asynchronous global -> shared copy of n keys (16-byte cp.async.cg, L2
+// only); completes at cp_async_wait_all().  n * sizeof(Key) % 16 == 0.
+template <typename Key, int T>
+__device__ __forceinline__ void cta_load_async(Key* __restrict__ s, const Key* __restrict__ g, uint32_t n) {
+    const uint32_t vecs = n * (uint32_t)sizeof(Key) / 16;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s);
+    for (uint32_t i = threadIdx.x; i < vecs; i += T)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + 16 * i),
+                     "l"(reinterpret_cast<const char*>(g) + 16ull * i)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ------------------------------------------------------------ L2 access --
 // Heap data is shared across SMs whose L1s are not coherent: all node reads

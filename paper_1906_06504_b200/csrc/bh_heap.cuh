@@ -45,6 +45,14 @@
 
 namespace bh {
 
+// Releases a delete server has deferred to its next op (kPubLane only).
+struct SvPending {
+    unsigned long long slot[5];
+    uint32_t rel[5];
+    uint32_t n;
+    unsigned long long pub;  // ticket whose hand-off flag is due (0 = none)
+};
+
 struct OpShared {
     unsigned long long op;
     unsigned long long nodes;
@@ -60,6 +68,11 @@ struct OpShared {
     uint32_t lrel, rrel;  // children release states
     uint32_t lastrel;
     uint32_t owned;
+    uint32_t serve;                // delete server: next ticket is a waiting delete
+    unsigned long long op_next;    // its op index
+    unsigned long long off_next;   // its out_pool offset
+    unsigned long long dbg_ts;
+    SvPending pd;
 };
 
 // Profile slots (BH_FLAG_PROFILE): SM cycles summed over ops by the leader.
@@ -92,6 +105,19 @@ enum ProfIdx {
     pfBuLevels, // BU climb levels
     pfSplitA,   // delete root split: refill half done (cycles from split start)
     pfSplitB,   // delete root split: children half done
+    pfDelServed,      // deletes whose top levels a delete server ran
+    pfDelServeHolds,  // root holds that served >= 1 waiting delete
+    pfSvSplit,  // delete server, per op: result + refill || H0 + level-2 claims
+    pfSvA,      //   refill half done (from op start)
+    pfSvB,      //   H0 + claim half done (from op start)
+    pfSvR1,     //   root + carried merges
+    pfSvR2,     //   lo + H1 merges
+    pfSvR3,     //   level-1 merges, lo2 write and release
+    pfSvNext,   //   next-waiter check and continuation hand-off
+    pfSvR1a,    //   r1: leader's merge half done (from r1 start)
+    pfSvR1b,    //   r1: second group's merge half done
+    pfSvR2a,    //   r2: leader's merge half done (from r2 start)
+    pfSvR2b,    //   r2: second group's merge half done
     kNumProf
 };
 
@@ -107,12 +133,12 @@ enum ProfIdx {
 #define BH_WAIT_NOTE(line) ((void)0)
 #define BH_WAIT_NOTE2(slot, w) ((void)0)
 #endif
-constexpr uint32_t kDbgWaitBase = 32;
+constexpr uint32_t kDbgWaitBase = 48;
 
 template <typename Key, int K, int T>
 struct HeapCta {
     static constexpr Key kMaxKey = KeyLimits<Key>::kMax;
-    static constexpr int kBufs = 8;
+    static constexpr int kBufs = 10;
     static constexpr uint32_t kNodeBytes = K * sizeof(Key);
     // prefetches are issued by warps other than the leader's
     static constexpr uint32_t kPfFirst = T > 64 ? 64 : 0;
@@ -127,7 +153,6 @@ struct HeapCta {
     OpShared* sh;
     Key* bufs;
     unsigned long long cnt[kNumCounters];
-    unsigned long long pf[kNumProf];
     unsigned long long cur_op;
     bool elide;
     bool record;
@@ -143,8 +168,6 @@ struct HeapCta {
         bufs = reinterpret_cast<Key*>(smem);
 #pragma unroll
         for (int i = 0; i < kNumCounters; ++i) cnt[i] = 0;
-#pragma unroll
-        for (int i = 0; i < kNumProf; ++i) pf[i] = 0;
         elide = (h.flags & BH_FLAG_ELIDE_MERGES) != 0;
         record = (h.flags & BH_FLAG_RECORD) != 0;
         prof = h.prof != nullptr;
@@ -176,9 +199,16 @@ struct HeapCta {
     __device__ __forceinline__ void count(int idx, unsigned long long v = 1) {
         if (leader()) cnt[idx] += v;
     }
-    __device__ __forceinline__ unsigned long long now() const { return prof ? clock64() : 0ull; }
+    __device__ __forceinline__ unsigned long long now() const {
+        if (!prof) return 0ull;
+        unsigned long long c;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)::"memory");  // not moved across memory ops
+        return c;
+    }
+    // profile slots go straight to global memory (a red per event, profiling
+    // builds only): no per-CTA register array
     __device__ __forceinline__ void pf_add(int idx, unsigned long long v) {
-        if (prof && leader()) pf[idx] += v;
+        if (prof && leader()) atomicAdd(&hv.prof[idx], v);
     }
     __device__ __forceinline__ void prefetch_node(unsigned long long slot) {
         if (slot > hv.slot_count) return;
@@ -228,24 +258,31 @@ struct HeapCta {
     // Queue slot line of ticket t: word 0 = hand-off flag (t<<1 granted,
     // t<<1|1 served by a combiner), word 1 = request word (t<<1|1 when the
     // waiter is a combinable insert), words 2-3 = its op index, words 4-9 =
-    // the combiner's response (rank, target slot, root sequence).
+    // the combiner's response (insert: rank, target slot, root sequence;
+    // delete: continuation slot, its release state), word 11 = request
+    // word of a servable delete (t<<1|1).
     __device__ __forceinline__ uint32_t* qline(unsigned long long t) const {
         return hv.root_flags + (t % kRootQueue) * kRootFlagStride;
     }
     // Returns true when a combiner ran this op's root phase instead of
     // granting the lock (combinable = a BU full-batch insert, see
     // serve_inserts).
-    __device__ bool root_lock(bool record_it = true, bool combinable = false) {
+    __device__ bool root_lock(bool record_it = true, bool combinable = false, bool del_req = false) {
         const unsigned long long t = atomicAdd(&hdr->root_tail, 1ull);
         uint32_t* f = qline(t);
-        if (combinable) {
+        if (combinable || del_req) {
             st_cg_u64(reinterpret_cast<unsigned long long*>(f + 2), cur_op);
-            state_store_release(f + 1, ((uint32_t)t << 1) | 1u);
+            state_store_release(f + (del_req ? 11 : 1), ((uint32_t)t << 1) | 1u);
         }
         const uint32_t granted = (uint32_t)t << 1;
-        Backoff b;
         uint32_t v;
-        while (((v = state_load(f)) & ~1u) != granted) { b.pause(); BH_WAIT_NOTE(__LINE__); }
+        if (del_req) {
+            QuickBackoff b;
+            while (((v = state_load(f)) & ~1u) != granted) { b.pause(); BH_WAIT_NOTE(__LINE__); }
+        } else {
+            Backoff b;
+            while (((v = state_load(f)) & ~1u) != granted) { b.pause(); BH_WAIT_NOTE(__LINE__); }
+        }
         sh->root_tk = t;
         if (v & 1u) return true;
         if (record_it) rec_lane(kEvAcq, 1);
@@ -437,11 +474,7 @@ struct HeapCta {
                     atomicAdd(&hv.counters[i], cnt[i]);
                 }
             }
-            if (prof) {
-#pragma unroll
-                for (int i = 0; i < kNumProf; ++i)
-                    if (pf[i]) atomicAdd(&hv.prof[i], pf[i]);
-            }
+
         }
     }
 
@@ -1164,7 +1197,11 @@ struct HeapCta {
 
     // refill_root_from(last), claim + copy + blank + release, by threads
     // [base, base + nthr) with barrier `bar`.  The refill batch lands in dst.
-    __device__ void refill_last(unsigned long long last, Key* dst, uint32_t base, uint32_t nthr, uint32_t bar) {
+    // `defer`: the last node stays claimed, blanked; the caller releases it
+    // as sh->lastrel after a barrier (the delete server, which waits on no
+    // claim until it has done so).
+    __device__ void refill_last(unsigned long long last, Key* dst, uint32_t base, uint32_t nthr, uint32_t bar,
+                                bool defer = false) {
         const uint32_t gt = threadIdx.x - base;
         for (;;) {
             if (gt == 0) lane_poll_last(last);
@@ -1188,11 +1225,366 @@ struct HeapCta {
             grp_sync(bar, nthr);
             if (sh->ok[2]) {
                 grp_fill_max<Key>(node(last), K, gt, nthr);
+                if (defer) return;
                 grp_sync(bar, nthr);
                 if (gt == 0) lane_unlock(last, sh->lastrel);
                 return;
             }
         }
+    }
+
+    // ================================================== delete serving ==
+    // Flat combining of deletes in the root queue lock (BU heaps, delete
+    // phase).  A delete holding the root with deletes queued behind it keeps
+    // the root and nodes 2-3 (claimed, in shared memory) and runs, for its own
+    // op and then each queued delete in ticket order, the reference's
+    // delete_min through levels 0 and 1: root result, refill from the last
+    // node, the level-0 and level-1 heapify steps (same merges, elisions, hi/lo
+    // choices and counters as heapify_down).  The heapify below level 1 --
+    // the carried batch and the claimed level-2 node -- is handed to the CTA
+    // of the next queued delete (through `mailbox` and its queue slot line),
+    // which is woken with it instead of the lock; the last continuation stays
+    // with the server.  Each op linearizes at its root step inside this root
+    // hold, in queue order, as its own root step would; levels 0-1 pass from
+    // one op to the next without a hand-off between SMs, which removes the
+    // two-step chain of section 6 from the top of the heap.
+    //
+    // Releases of an op (its last node, level-2 nodes, the hand-off flag of
+    // the continuation) are deferred to the start of the next op and issued by
+    // one lane (kPubLane) behind a single fence, while lane 0 polls the next
+    // refill.  Deadlock freedom as in the reference: the server waits on a
+    // claim only in the split of an op (level-2 children), and by then every
+    // node it holds besides levels 0-1 has been released by kPubLane, which
+    // waits on nothing.
+    static constexpr unsigned long long kServeMin = 64;  // last node stays below level 5
+    static constexpr uint32_t kRefBase = T >= 256 ? 64 : 32;  // refill group: [kRefBase, T/2)
+    static constexpr uint32_t kHalfT = T / 2;
+    static constexpr uint32_t kPubLane = T >= 256 ? 32 : 1;  // outside the refill group
+
+    __device__ __forceinline__ Key* mbox(unsigned long long t) const {
+        return static_cast<Key*>(hv.mailbox) + (t % kRootQueue) * (unsigned long long)K;
+    }
+
+    // Leader or kPubLane: is ticket t a delete that posted a serve request?
+    __device__ bool waiting_delete(unsigned long long t, unsigned long long& op) {
+        uint32_t* f = qline(t);
+        if (state_load(f + 11) != (((uint32_t)t << 1) | 1u)) return false;
+        op = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 2));
+        return true;
+    }
+
+    __device__ __forceinline__ void pend(unsigned long long slot, uint32_t rel) {
+        if (threadIdx.x == kPubLane) {
+            sh->pd.slot[sh->pd.n] = slot;
+            sh->pd.rel[sh->pd.n] = rel;
+            ++sh->pd.n;
+        }
+    }
+
+    // kPubLane: the previous op's releases, one fence for all of them.
+    __device__ void sv_flush(SvPending& pd) {
+        bool fenced = false;
+        for (uint32_t i = 0; i < pd.n; ++i) {
+            if (!fenced) state_release(st(pd.slot[i]), kInUse, pd.rel[i]);
+            else state_release_relaxed(st(pd.slot[i]), kInUse, pd.rel[i]);
+            fenced = true;
+        }
+        if (pd.pub) {
+            if (!fenced) __threadfence();
+            state_store_relaxed(qline(pd.pub), ((uint32_t)pd.pub << 1) | 1u);
+        }
+        pd.n = 0;
+        pd.pub = 0;
+    }
+
+    // Two independent half merges, side by side on the two thread groups when
+    // they fit (HalfShape::kPair), else one after the other.  No barrier.
+    template <bool S1, bool S2, bool G2 = false>
+    __device__ __forceinline__ void two_halves(const Key* A1, const Key* B1, Key* o1, bool do1, const Key* A2,
+                                               const Key* B2, Key* o2, bool do2) {
+        if constexpr (HalfShape<K, T>::kPair) {
+            constexpr uint32_t kT = HalfShape<K, T>::kThreads;
+            if (threadIdx.x < kT) {
+                if (do1) cta_merge_half<Key, K, T, S1, false>(A1, B1, o1, threadIdx.x, kT);
+            } else if (threadIdx.x < 2 * kT) {
+                if (do2) cta_merge_half<Key, K, T, S2, G2>(A2, B2, o2, threadIdx.x - kT, kT);
+            }
+        } else {
+            if (do1) cta_merge_half<Key, K, T, S1, false>(A1, B1, o1, threadIdx.x, T);
+            if (do2) cta_merge_half<Key, K, T, S2, G2>(A2, B2, o2, threadIdx.x, T);
+        }
+    }
+
+    // One delete (ticket t) through levels 0 and 1.  Buffers n1/n2/n3 hold
+    // nodes 1-3 (in and out).  Returns the continuation node (0 = heapify
+    // done) and its release state; its carried batch is in mbox(t + 1) when
+    // sh->serve (the next ticket is served next), else in buf(cbuf).  pd:
+    // releases due (in) / deferred by this op (out).  Schedule (8 half
+    // merges, two at a time):
+    //   split  refill (claim, copy, blank) || H0, claim hi1's children, lo0
+    //   r1     new root || carried        (halves of merge(refill, H0))
+    //   r2     H1 || lo2 -> HBM           (halves of merge(L2, R2))
+    //   r3     new hi1 || next carried    (halves of merge(carried, H1))
+    __device__ unsigned long long serve_one(unsigned long long opi, unsigned long long off, unsigned long long seq,
+                                            unsigned long long nodes, unsigned long long t, int& n1, int& n2,
+                                            int& n3, int& cbuf, uint32_t& crel) {
+        const unsigned long long ts0 = now();
+        Key* out = static_cast<Key*>(rv.out_pool) + off;
+        if (threadIdx.x >= kHalfT) {  // the result: the root's k keys (B group: no fences follow)
+            const uint4* sv = reinterpret_cast<const uint4*>(buf(n1));
+            uint4* gv = reinterpret_cast<uint4*>(out);
+            for (uint32_t i = threadIdx.x - kHalfT; i < kNodeBytes / 16; i += kHalfT) __stcg(gv + i, sv[i]);
+        }
+        count(cDeletes);
+        if (leader() && buf(n1)[K - 1] == kMaxKey)
+            atomicOr(&hdr->error_flags, (unsigned long long)kErrSentinelEscaped);
+        status(opi, BH_OK, K, seq);
+        if (threadIdx.x >= 8 && threadIdx.x < 8 + kRefillAhead && nodes > threadIdx.x - 8 + 5) {
+            const unsigned long long slot = slot_for_rank(nodes - 1 - (threadIdx.x - 8));
+            const char* a = reinterpret_cast<const char*>(node(slot));
+            for (uint32_t off = 0; off < kNodeBytes; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(st(slot)));
+        }
+        uint32_t used = (1u << n1) | (1u << n2) | (1u << n3);
+        auto alloc = [&]() {
+            const int b = __ffs(~used) - 1;
+            used |= 1u << b;
+            return b;
+        };
+        const Key* L = buf(n2);
+        const Key* R = buf(n3);
+        // level-0 children decision (independent of the refill)
+        const bool lempty = L[0] == kMaxKey, rempty = R[0] == kMaxKey;
+        bool hi_left, mc0 = false, el0 = false;
+        if (lempty) {
+            hi_left = false;
+        } else if (rempty) {
+            hi_left = true;
+        } else if (elide && !needs_merge_full<Key, K>(L, R)) {
+            el0 = true;
+            hi_left = L[K - 1] <= R[0];  // tie fix of heap.cpp:628-636
+        } else {
+            hi_left = !(L[K - 1] > R[K - 1]);
+            mc0 = true;
+        }
+        const int rf = alloc(), l2 = alloc(), r2 = alloc();
+        const int h0 = mc0 ? alloc() : -1;
+        const int nlo = mc0 ? alloc() : (hi_left ? n3 : n2);  // the lo child's new batch
+        const unsigned long long hi1 = hi_left ? 2 : 3;
+        const unsigned long long c2l = 2 * hi1, c2r = 2 * hi1 + 1;
+        const unsigned long long last = slot_for_rank(nodes);
+        // refill (claim, copy, blank; released with the next op's flush)
+        // || H0, the claim of hi1's children, lo0
+        // warps below kRefBase stay out of the refill group: the leader's bookkeeping
+        // and kPubLane's flush + next-waiter lookup run beside it
+        if (threadIdx.x < kRefBase) {
+            if (threadIdx.x == kPubLane) {
+#ifndef BH_EXP_LATEFLUSH
+                sv_flush(sh->pd);
+#endif
+                unsigned long long nop = 0;
+                const bool more = nodes - 1 >= kServeMin && waiting_delete(t + 1, nop);
+                sh->serve = more;
+                sh->op_next = nop;
+                if (more) sh->off_next = rv.ops[nop].offset;
+            }
+        } else if (threadIdx.x < kHalfT) {
+            refill_last(last, buf(rf), kRefBase, kHalfT - kRefBase, 1, true);
+            if (prof && threadIdx.x == kRefBase) atomicAdd(&hv.prof[pfSvA], now() - ts0);
+        } else if (mc0) {
+            // both halves of merge(L, R): H0 and the lo child's new batch
+            cta_merge_half<Key, K, T, false, false>(L, R, buf(h0), threadIdx.x - kHalfT, kHalfT);
+            cta_merge_half<Key, K, T, true, false>(L, R, buf(nlo), threadIdx.x - kHalfT, kHalfT);
+            if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvB], now() - ts0);
+        }
+        if (prof && threadIdx.x == T - 1) sh->dbg_ts = seq;
+        __syncthreads();
+        if (prof && leader() && sh->dbg_ts != seq) atomicAdd(&hv.prof[pfSvR2a], 1ull);
+        const unsigned long long ts1 = now();
+        pf_add(pfSvSplit, ts1 - ts0);
+#ifdef BH_EXP_LATEFLUSH
+        if (threadIdx.x == kPubLane) sv_flush(sh->pd);
+#endif
+        const bool handoff = sh->serve != 0;
+        pend(last, sh->lastrel);
+        const Key* RF = buf(rf);
+
+        // ---- level 0: cur = the refill ----
+        const Key cmax = RF[K - 1];
+        bool stop0 = lempty && rempty;
+        if (!stop0 && cmax <= (lempty ? kMaxKey : L[0]) && cmax <= (rempty ? kMaxKey : R[0])) {
+            count(cEarlyStops);
+            stop0 = true;
+        }
+        if (stop0) {  // the refill is the new root, levels 1-2 unchanged
+            n1 = rf;
+            return 0;
+        }
+        if (mc0) count(cMerges);
+        else if (el0) count(cElided);
+        const int hd0 = mc0 ? h0 : (hi_left ? n2 : n3);
+        const bool mcur0 = !(elide && !needs_merge_full<Key, K>(RF, buf(hd0)));
+        count(mcur0 ? cMerges : cElided);
+        count(cVisits);
+        // live: rf, hd0, nlo, l2, r2
+        used = (1u << rf) | (1u << hd0) | (1u << nlo) | (1u << l2) | (1u << r2);
+        int nr, ca;
+        if (mcur0) {
+            nr = alloc();
+            ca = alloc();
+            two_halves<false, true>(RF, buf(hd0), buf(nr), true, RF, buf(hd0), buf(ca), true);
+        } else {  // full inversion: the hi batch moves up, the refill goes down
+            nr = hd0;
+            ca = rf;
+        }
+        pf_add(pfSvR1, now() - ts1);
+        // hi1's children: the one claim the server may wait on (for the
+        // continuation of the previous op on the same side), as late as
+        // possible; nothing but levels 0-1 is held here
+        const unsigned long long tc = now();
+        acquire_children(hi1, buf(l2), buf(r2));
+        const unsigned long long ts2 = now();
+        pf_add(pfSvR1b, ts2 - tc);
+        const uint32_t lk2 = sh->lk, rk2 = sh->rk, lrel2 = sh->lrel, rrel2 = sh->rrel;
+
+        // ---- level 1: cur = carried batch at hi1, children claimed above ----
+        used = (1u << nr) | (1u << nlo) | (1u << ca) | (1u << l2) | (1u << r2);
+        const Key* L2 = buf(l2);
+        const Key* R2 = buf(r2);
+        const Key* CA = buf(ca);
+        const bool le2 = !lk2 || L2[0] == kMaxKey, re2 = !rk2 || R2[0] == kMaxKey;
+        const Key cmax1 = CA[K - 1];
+        bool stop1 = le2 && re2;
+        if (!stop1 && cmax1 <= (le2 ? kMaxKey : L2[0]) && cmax1 <= (re2 ? kMaxKey : R2[0])) {
+            count(cEarlyStops);
+            stop1 = true;
+        }
+        unsigned long long cont = 0;
+        int nhi;
+        if (stop1) {
+            nhi = ca;
+            if (lk2) pend(c2l, lrel2);
+            if (rk2) pend(c2r, rrel2);
+        } else {
+            bool hl1, mc1 = false;
+            if (le2) {
+                hl1 = false;
+            } else if (re2) {
+                hl1 = true;
+            } else if (elide && !needs_merge_full<Key, K>(L2, R2)) {
+                count(cElided);
+                hl1 = L2[K - 1] <= R2[0];
+            } else {
+                hl1 = !(L2[K - 1] > R2[K - 1]);
+                mc1 = true;
+                count(cMerges);
+            }
+            const unsigned long long hi2 = hl1 ? c2l : c2r, lo2 = hl1 ? c2r : c2l;
+            const uint32_t lo2_locked = hl1 ? rk2 : lk2;
+            const uint32_t hi2_rel = hl1 ? lrel2 : rrel2, lo2_rel = hl1 ? rrel2 : lrel2;
+            const int h1 = mc1 ? alloc() : -1;
+            if (mc1) {
+                // H1 || lo2's batch (second half of merge(L2, R2)) -> HBM
+                two_halves<false, true, true>(L2, R2, buf(h1), true, L2, R2, node(lo2), true);
+                __syncthreads();
+            }
+            const unsigned long long ts3 = now();
+            pf_add(pfSvR2, ts3 - ts2);
+            const int hd1 = mc1 ? h1 : (hl1 ? l2 : r2);
+            const bool mcur1 = !(elide && !needs_merge_full<Key, K>(CA, buf(hd1)));
+            count(mcur1 ? cMerges : cElided);
+            count(cVisits);
+            // the carried batch goes straight to the next ticket's mailbox
+            // when that op is served next, else it stays here
+            if (mcur1) {
+                nhi = alloc();
+                cbuf = alloc();
+                if (handoff)
+                    two_halves<false, true, true>(CA, buf(hd1), buf(nhi), true, CA, buf(hd1), mbox(t + 1), true);
+                else
+                    two_halves<false, true>(CA, buf(hd1), buf(nhi), true, CA, buf(hd1), buf(cbuf), true);
+            } else {
+                nhi = hd1;
+                cbuf = ca;
+                if (handoff) cta_store<Key, T>(mbox(t + 1), CA, K);
+            }
+            if (lo2_locked) pend(lo2, lo2_rel);  // merged above, or unchanged
+            cont = hi2;
+            crel = hi2_rel;
+            pf_add(pfSvR3, now() - ts3);
+        }
+        __syncthreads();
+        n1 = nr;
+        if (hi1 == 2) {
+            n2 = nhi;
+            n3 = nlo;
+        } else {
+            n3 = nhi;
+            n2 = nlo;
+        }
+        return cont;
+    }
+
+    // Root held (ticket sh->root_tk), gate passed, buf(0) = root batch,
+    // partial buffer empty, the next ticket a waiting delete.
+    __device__ void serve_deletes(unsigned long long opi, unsigned long long seq, unsigned long long nodes) {
+        int n1 = 0, n2 = 1, n3 = 2;
+        acquire_children(1, buf(n2), buf(n3));
+        const uint32_t rel2 = sh->lrel, rel3 = sh->rrel;
+        unsigned long long t = sh->root_tk, op = opi, served = 0, off = rv.ops[opi].offset;
+        int cbuf = -1;
+        uint32_t crel = kAvail;
+        unsigned long long cont = 0;
+        if (threadIdx.x == kPubLane) {
+            sh->pd.n = 0;
+            sh->pd.pub = 0;
+        }
+        for (;;) {
+            cont = serve_one(op, off, seq, nodes, t, n1, n2, n3, cbuf, crel);
+            const unsigned long long tn = now();
+            ++seq;
+            --nodes;
+            const bool more = sh->serve != 0;
+            const unsigned long long nop = sh->op_next;
+            const unsigned long long noff = sh->off_next;
+            __syncthreads();  // everyone has read sh->serve / op_next
+            if (!more) break;
+            // the waiter of ticket t+1 takes this op's continuation (its
+            // carried batch is in mbox(t+1)); its own op is served next.  The
+            // flag goes out with the next op's flush.
+            if (threadIdx.x == kPubLane) {
+                unsigned long long* f = reinterpret_cast<unsigned long long*>(qline(t + 1));
+                st_cg_u64(f + 2, cont);
+                st_cg_u64(f + 3, crel);
+                atomicAdd(&hdr->deleters, 1ull);  // op t+1 is in the delete phase
+            }
+            if (threadIdx.x == kPubLane) sh->pd.pub = t + 1;
+            op = nop;
+            off = noff;
+            ++t;
+            ++served;
+            pf_add(pfSvNext, now() - tn);
+        }
+        // write the top levels back, then release everything and the root
+        cta_store<Key, T>(node(1), buf(n1), K);
+        cta_store<Key, T>(node(2), buf(n2), K);
+        cta_store<Key, T>(node(3), buf(n3), K);
+        if (leader()) {
+            st_cg_u64(&hdr->node_count, nodes);
+            st_cg_u64(&hdr->delete_count, seq);
+        }
+        __syncthreads();
+        pend(2, rel2);
+        if (threadIdx.x == kPubLane) {
+            sv_flush(sh->pd);
+            state_release_relaxed(st(3), kInUse, rel3);
+            sh->root_tk = t;
+            state_store_relaxed(qline(t + 1), (uint32_t)(t + 1) << 1);  // root_unlock
+        }
+        pf_add(pfDelServed, served);
+        pf_add(pfDelServeHolds, served ? 1 : 0);
+        if (cont) heapify_down(cbuf, 0, false, cont, crel);
+        if (leader()) gate_leave(false);
     }
 
     __device__ void do_delete(unsigned long long opi, const bh_op& o) {
@@ -1202,9 +1594,14 @@ struct HeapCta {
             uint32_t gated = 0;
             if (hv.variant == BH_BU) {
                 // BU phase gate: a delete that will heapify (>= 2 nodes) waits
-                // until no bottom-up climb is in flight
+                // until no bottom-up climb is in flight.  The request lets a
+                // delete server ahead in the queue run this op (serve_deletes).
+                const bool can_post = T >= 128 && !record && (hv.flags & kDbgNoDelServe) == 0;
                 for (;;) {
-                    root_lock(false);
+                    if (root_lock(false, false, can_post)) {
+                        gated = 2;  // served: counted in the gate by the server
+                        break;
+                    }
                     const unsigned long long nodes_now = ld_cg_u64(&hdr->node_count);
                     if (nodes_now < 2) break;
                     if (gate_try(false)) {
@@ -1222,6 +1619,24 @@ struct HeapCta {
         }
         const unsigned long long t1 = now();
         __syncthreads();
+        if (sh->owned == 2) {
+            // a delete server ran this op's top levels and wrote its result;
+            // this CTA runs the continuation of the op served before it
+            const unsigned long long tk = sh->root_tk;
+            const unsigned long long* f = reinterpret_cast<const unsigned long long*>(qline(tk));
+            const unsigned long long cont = ld_cg_u64(f + 2);  // words 4-5
+            const uint32_t crel = (uint32_t)(ld_cg_u64(f + 3) & 0xFFFFFFFFu);  // word 6
+            if (cont) {
+                // the carried batch travels while the node's children are claimed
+                cta_load_async<Key, T>(buf(0), mbox(tk), K);
+                acquire_children(cont, buf(1), buf(2));
+                cp_async_wait_all();
+                __syncthreads();
+                heapify_down(0, t1, true, cont, crel);
+            }
+            if (leader()) gate_leave(false);
+            return;
+        }
         const bool gated = sh->owned != 0;
         // the root batch, read in the same round trip as the header
         Key* cur_s = buf(0);
@@ -1270,6 +1685,19 @@ struct HeapCta {
             return;
         }
 
+        // delete serving: with waiting deletes queued behind, this CTA keeps
+        // the root and runs their top levels too
+        if (T >= 128 && gated && plen == 0 && nodes >= kServeMin && !record && (hv.flags & kDbgNoDelServe) == 0) {
+            if (leader()) {
+                unsigned long long nop = 0;
+                sh->serve = waiting_delete(sh->root_tk + 1, nop);
+            }
+            __syncthreads();
+            if (sh->serve) {
+                serve_deletes(opi, seq, nodes);
+                return;
+            }
+        }
         cta_store<Key, T>(out, cur_s, K);  // the result: the root's k keys
         if (leader()) {
             if (cur_s[K - 1] == kMaxKey)
@@ -1357,14 +1785,17 @@ struct HeapCta {
     // claim round trip and H merge run in the shadow of the second halves.
     // Lock order, states and released contents are the reference's.
     // `pre`: the root's children are already claimed, in buf(1) and buf(2).
-    __device__ void heapify_down(int ci, unsigned long long t_root, bool pre) {
+    // `start`/`start_rel`: a served delete's continuation starts below the
+    // levels its server ran, at a node the server claimed (serve_one).
+    __device__ void heapify_down(int ci, unsigned long long t_root, bool pre, unsigned long long start = 1,
+                                 uint32_t start_rel = kAvail) {
         constexpr bool kSplit = T >= 64;
         constexpr uint32_t kHalf = kSplit ? T / 2 : T;
         // upper-half lane with no claim duty (acquire_children polls with its
         // first two lanes)
         constexpr uint32_t kRelLane = kSplit ? (T >= 128 ? kHalf + 32 : kHalf + 2) : 0;
-        unsigned long long cur = 1;
-        uint32_t cur_rel = kAvail;
+        unsigned long long cur = start;
+        uint32_t cur_rel = start_rel;
         const unsigned long long t_start = now();
         auto free_buf = [](uint32_t used) { return __ffs(~used) - 1; };
         int li, ri;
@@ -1540,7 +1971,7 @@ template <typename Key, int K>
 struct KernelCfg {
     static constexpr int kWant = K / BH_THREADS_DIV;
     static constexpr int kThreads = kWant < 32 ? 32 : (kWant > BH_THREADS_CAP ? BH_THREADS_CAP : kWant);
-    static constexpr uint32_t kSmem = 8u * K * sizeof(Key) + 64;  // + window over-read pad
+    static constexpr uint32_t kSmem = 10u * K * sizeof(Key) + 64;  // + window over-read pad
 };
 
 }  // namespace bh

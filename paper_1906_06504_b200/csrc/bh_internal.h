@@ -23,8 +23,8 @@ constexpr uint32_t kStateStride = 8;  // uint32 words
 // Root queue lock: one flag per waiter slot, each on its own 128-byte line.
 constexpr uint32_t kRootQueue = 4096;
 constexpr uint32_t kRootFlagStride = 32;  // uint32 words
-// Profile buffer: 32 counters + 4 debug words per CTA (up to 4096 CTAs).
-constexpr uint32_t kProfWords = 32 + 4 * 4096;
+// Profile buffer: 48 counters + 4 debug words per CTA (up to 4096 CTAs).
+constexpr uint32_t kProfWords = 48 + 4 * 4096;
 
 // Debug-only protocol toggles (bh_create flags, not in the public header).
 constexpr uint32_t kDbgSeqRefill = 0x100;       // reference refill order in every delete
@@ -32,6 +32,7 @@ constexpr uint32_t kDbgWriteUnderRoot = 0x200;  // BU target written before the 
 constexpr uint32_t kDbgSerialLanes = 0x400;     // claim children one after the other
 constexpr uint32_t kDbgNoCombine = 0x800;       // no insert combining in the root queue lock
 constexpr uint32_t kDbgParkClimb = 0x1000;      // reference BU climb (fenced park, reload on re-take)
+constexpr uint32_t kDbgNoDelServe = 0x2000;     // no delete serving in the root queue lock
 
 // Heap header, root-lock guarded (reference heap.hpp:173-177).  One cache
 // line; the partial buffer follows in its own allocation.
@@ -91,6 +92,7 @@ struct HeapView {
     uint32_t* root_flags;    // kRootQueue * kRootFlagStride
     Header* hdr;
     void* partial;           // k keys
+    void* mailbox;           // kRootQueue * k keys: carried batches of served deletes (BU)
     unsigned long long* counters;
     unsigned long long* prof;  // non-null on BH_FLAG_PROFILE handles
     unsigned long long slot_count;

@@ -278,12 +278,14 @@ class GeneralizedHeap:
                       "del_ops", "del_root_wait", "del_root_hold", "del_rest", "child_wait",
                       "levels", "cta_cycles", "rs_head", "rs_child", "rs_last", "rs_load",
                       "rs_fill", "lv_acq", "lv_load", "lv_merge", "lv_rel", "served",
-                      "serve_holds", "bu_parent", "bu_retake", "bu_levels", "split_a", "split_b")
+                      "serve_holds", "bu_parent", "bu_retake", "bu_levels", "split_a", "split_b",
+                      "del_served", "del_serve_holds", "sv_split", "sv_a", "sv_b", "sv_r1", "sv_r2",
+                      "sv_r3", "sv_next", "sv_r1a", "sv_r1b", "sv_r2a", "sv_r2b")
 
     def profile(self, reset: bool = True) -> dict:
         """SM-cycle profile of a BH_FLAG_PROFILE heap (see bh_profile)."""
-        buf = (C.c_uint64 * 32)()
-        _raise(L.lib().bh_profile(self._h, buf, 32, int(reset)))
+        buf = (C.c_uint64 * 48)()
+        _raise(L.lib().bh_profile(self._h, buf, 48, int(reset)))
         return dict(zip(self.PROFILE_FIELDS, (int(v) for v in buf)))
 
     def info(self) -> dict:
