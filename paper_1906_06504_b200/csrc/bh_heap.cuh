@@ -1197,11 +1197,7 @@ struct HeapCta {
 
     // refill_root_from(last), claim + copy + blank + release, by threads
     // [base, base + nthr) with barrier `bar`.  The refill batch lands in dst.
-    // `defer`: the last node stays claimed, blanked; the caller releases it
-    // as sh->lastrel after a barrier (the delete server, which waits on no
-    // claim until it has done so).
-    __device__ void refill_last(unsigned long long last, Key* dst, uint32_t base, uint32_t nthr, uint32_t bar,
-                                bool defer = false) {
+    __device__ void refill_last(unsigned long long last, Key* dst, uint32_t base, uint32_t nthr, uint32_t bar) {
         const uint32_t gt = threadIdx.x - base;
         for (;;) {
             if (gt == 0) lane_poll_last(last);
@@ -1225,7 +1221,6 @@ struct HeapCta {
             grp_sync(bar, nthr);
             if (sh->ok[2]) {
                 grp_fill_max<Key>(node(last), K, gt, nthr);
-                if (defer) return;
                 grp_sync(bar, nthr);
                 if (gt == 0) lane_unlock(last, sh->lastrel);
                 return;
@@ -1249,13 +1244,14 @@ struct HeapCta {
     // one op to the next without a hand-off between SMs, which removes the
     // two-step chain of section 6 from the top of the heap.
     //
-    // Releases of an op (its last node, level-2 nodes, the hand-off flag of
-    // the continuation) are deferred to the start of the next op and issued by
-    // one lane (kPubLane) behind a single fence, while lane 0 polls the next
-    // refill.  Deadlock freedom as in the reference: the server waits on a
-    // claim only in the split of an op (level-2 children), and by then every
-    // node it holds besides levels 0-1 has been released by kPubLane, which
-    // waits on nothing.
+    // Releases of an op's level-2 nodes and the hand-off flag of its
+    // continuation are deferred to the start of the next op and issued by one
+    // lane (kPubLane, outside the refill group) behind a single fence.
+    // Deadlock freedom as in the reference: the server waits on a claim only
+    // for hi1's children, after its refill has released the last node, and
+    // the level-2 nodes of the previous op are released by kPubLane, which
+    // waits on nothing; so the server then holds only nodes 1-3, which no
+    // other op waits for while holding anything.
     static constexpr unsigned long long kServeMin = 64;  // last node stays below level 5
     static constexpr uint32_t kRefBase = T >= 256 ? 64 : 32;  // refill group: [kRefBase, T/2)
     static constexpr uint32_t kHalfT = T / 2;
@@ -1389,7 +1385,8 @@ struct HeapCta {
                 if (more) sh->off_next = rv.ops[nop].offset;
             }
         } else if (threadIdx.x < kHalfT) {
-            refill_last(last, buf(rf), kRefBase, kHalfT - kRefBase, 1, true);
+            // released here, before the server waits on any claim (below)
+            refill_last(last, buf(rf), kRefBase, kHalfT - kRefBase, 1);
             if (prof && threadIdx.x == kRefBase) atomicAdd(&hv.prof[pfSvA], now() - ts0);
         } else if (mc0) {
             // both halves of merge(L, R): H0 and the lo child's new batch
@@ -1406,7 +1403,6 @@ struct HeapCta {
         if (threadIdx.x == kPubLane) sv_flush(sh->pd);
 #endif
         const bool handoff = sh->serve != 0;
-        pend(last, sh->lastrel);
         const Key* RF = buf(rf);
 
         // ---- level 0: cur = the refill ----
