@@ -1248,10 +1248,11 @@ struct HeapCta {
     // continuation are deferred to the start of the next op and issued by one
     // lane (kPubLane, outside the refill group) behind a single fence.
     // Deadlock freedom as in the reference: the server waits on a claim only
-    // for hi1's children, after its refill has released the last node, and
-    // the level-2 nodes of the previous op are released by kPubLane, which
-    // waits on nothing; so the server then holds only nodes 1-3, which no
-    // other op waits for while holding anything.
+    // for hi1's children; its refill beside that claim never waits while it
+    // holds the last node, and the level-2 nodes of the previous op are
+    // released by kPubLane, which waits on nothing; so across the wait the
+    // server holds only nodes 1-3, which no other op waits for while holding
+    // anything.
     static constexpr unsigned long long kServeMin = 64;  // last node stays below level 5
     static constexpr uint32_t kRefBase = T >= 256 ? 64 : 32;  // refill group: [kRefBase, T/2)
     static constexpr uint32_t kHalfT = T / 2;
@@ -1388,11 +1389,20 @@ struct HeapCta {
             // released here, before the server waits on any claim (below)
             refill_last(last, buf(rf), kRefBase, kHalfT - kRefBase, 1);
             if (prof && threadIdx.x == kRefBase) atomicAdd(&hv.prof[pfSvA], now() - ts0);
-        } else if (mc0) {
-            // both halves of merge(L, R): H0 and the lo child's new batch
-            cta_merge_half<Key, K, T, false, false>(L, R, buf(h0), threadIdx.x - kHalfT, kHalfT);
-            cta_merge_half<Key, K, T, true, false>(L, R, buf(nlo), threadIdx.x - kHalfT, kHalfT);
+        } else {
+            // both halves of merge(L, R): H0 and the lo child's new batch,
+            // then hi1's children: the one claim the server may wait on (for
+            // the continuation of the previous op on the same side), issued
+            // last.  The refill beside it never waits while holding the last
+            // node, so nothing but nodes 1-3 is held across this wait.
+            if (mc0) {
+                cta_merge_half<Key, K, T, false, false>(L, R, buf(h0), threadIdx.x - kHalfT, kHalfT);
+                cta_merge_half<Key, K, T, true, false>(L, R, buf(nlo), threadIdx.x - kHalfT, kHalfT);
+            }
             if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvB], now() - ts0);
+            const unsigned long long tc = now();
+            acquire_children(hi1, buf(l2), buf(r2), kHalfT, kHalfT, 2);
+            if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvR1b], now() - tc);
         }
         if (prof && threadIdx.x == T - 1) sh->dbg_ts = seq;
         __syncthreads();
@@ -1412,7 +1422,10 @@ struct HeapCta {
             count(cEarlyStops);
             stop0 = true;
         }
+        const uint32_t lk2 = sh->lk, rk2 = sh->rk, lrel2 = sh->lrel, rrel2 = sh->rrel;
         if (stop0) {  // the refill is the new root, levels 1-2 unchanged
+            if (lk2) pend(c2l, lrel2);
+            if (rk2) pend(c2r, rrel2);
             n1 = rf;
             return 0;
         }
@@ -1434,14 +1447,8 @@ struct HeapCta {
             ca = rf;
         }
         pf_add(pfSvR1, now() - ts1);
-        // hi1's children: the one claim the server may wait on (for the
-        // continuation of the previous op on the same side), as late as
-        // possible; nothing but levels 0-1 is held here
-        const unsigned long long tc = now();
-        acquire_children(hi1, buf(l2), buf(r2));
+        __syncthreads();
         const unsigned long long ts2 = now();
-        pf_add(pfSvR1b, ts2 - tc);
-        const uint32_t lk2 = sh->lk, rk2 = sh->rk, lrel2 = sh->lrel, rrel2 = sh->rrel;
 
         // ---- level 1: cur = carried batch at hi1, children claimed above ----
         used = (1u << nr) | (1u << nlo) | (1u << ca) | (1u << l2) | (1u << r2);
