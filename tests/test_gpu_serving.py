@@ -1,0 +1,92 @@
+"""Delete serving (bh_heap.cuh serve_deletes): a BU delete holding the root
+with deletes queued behind it runs their levels 0-1 from shared memory and
+hands each continuation to the next waiter.  Compared with the one-root-hold-
+per-delete path (kDbgNoDelServe): the same deleted batches in the same order
+(each op still linearizes at its root step, in queue order), a valid heap
+after a partial phase (properties 1-2, multiset), and a heap that keeps
+working for later inserts and deletes."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1906_06504_b200 import GeneralizedHeap, Variant, make_ops, phase_ops
+
+pytestmark = pytest.mark.gpu
+NO_DEL_SERVE = 0x2000
+
+
+def _deleted(heap, n_ops, k):
+    d = heap.run_ops(phase_ops(1, n_ops * k, k), np.zeros(0, np.uint32), n_ops * k)
+    assert np.all(d.status == 0)
+    order = np.argsort(d.seq, kind="stable")
+    out = d.out.reshape(n_ops, k)[order]
+    lens = d.lens[order]
+    return np.concatenate([out[i, :lens[i]] for i in range(n_ops)]).astype(np.uint64)
+
+
+@pytest.mark.parametrize("k", [256, 1024, 2048])
+def test_serving_engages_and_drains_sorted(k):
+    n = 1 << 20
+    keys = O.generate_keys(n, 11)
+    served = {}
+    for flags in (0, NO_DEL_SERVE):
+        heap = GeneralizedHeap(Variant.BU, k, n // k + 64, key_bits=32, profile=True, debug_flags=flags)
+        assert np.all(heap.run_ops(phase_ops(0, n, k), keys.astype(np.uint32), 0).status == 0)
+        heap.profile(reset=True)
+        got = _deleted(heap, n // k, k)
+        served[flags] = heap.profile()["del_served"]
+        assert np.array_equal(got, O.sort_u64(keys))
+        assert heap.peek_stats().node_count == 0
+        heap.close()
+    assert served[0] > (n // k) // 2  # most deletes were served
+    assert served[NO_DEL_SERVE] == 0
+
+
+@pytest.mark.parametrize("k", [256, 1024])
+def test_serving_partial_phase_leaves_a_valid_heap(k):
+    n = (1 << 19) + 5 * k
+    keys = O.generate_keys(n, 12).astype(np.uint64)
+    heap = GeneralizedHeap(Variant.BU, k, 2 * (n // k) + 64, key_bits=32)
+    assert np.all(heap.run_ops(phase_ops(0, n, k), keys.astype(np.uint32), 0).status == 0)
+    m = (n // k) // 2
+    srt = np.sort(keys)
+    assert np.array_equal(_deleted(heap, m, k), srt[:m * k])
+    rep = heap.check_invariants()
+    assert rep.ok, rep.detail
+    assert np.array_equal(np.sort(heap.collect_resident().astype(np.uint64)), srt[m * k:])
+    # the heap keeps working: more inserts, then the whole drain
+    more = O.generate_keys(64 * k, 13).astype(np.uint64)
+    ins = heap.run_ops(phase_ops(0, more.size, k), more.astype(np.uint32), 0)
+    assert np.all(ins.status == 0)
+    rest = np.sort(np.concatenate([srt[m * k:], more]))
+    assert np.array_equal(_deleted(heap, rest.size // k, k), rest)
+
+
+def test_serving_with_interleaved_inserts_conserves_keys():
+    """Delete runs broken by inserts (BU phase gate included): servers stop at an insert in the queue;
+    every key inserted comes out once, invariants hold at quiescence."""
+    k, n = 1024, 1 << 19
+    keys = O.generate_keys(2 * n, 14).astype(np.uint64)
+    heap = GeneralizedHeap(Variant.BU, k, 2 * (2 * n // k) + 64, key_bits=32)
+    assert np.all(heap.run_ops(phase_ops(0, n, k), keys[:n].astype(np.uint32), 0).status == 0)
+    # 3 deletes, 1 insert, repeated
+    n_ins = (n // k) // 2
+    kinds, lens, offs = [], [], []
+    di = 0
+    for i in range(n_ins):
+        for _ in range(3):
+            kinds.append(1)
+            lens.append(0)
+            offs.append(di * k)
+            di += 1
+        kinds.append(0)
+        lens.append(k)
+        offs.append(n + i * k)
+    ops = make_ops(np.array(kinds, np.uint32), np.array(lens, np.uint32), np.array(offs, np.uint64))
+    r = heap.run_ops(ops, keys.astype(np.uint32), di * k)
+    assert set(np.unique(r.status).tolist()) <= {0, 3}
+    rep = heap.check_invariants()
+    assert rep.ok, rep.detail
+    out = [r.out[o["offset"]:o["offset"] + r.lens[i]] for i, o in enumerate(ops) if o["kind"] == 1]
+    got = np.sort(np.concatenate(out + [heap.collect_resident()]).astype(np.uint64))
+    assert np.array_equal(got, np.sort(keys[:n + n_ins * k]))
