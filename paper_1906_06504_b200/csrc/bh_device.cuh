@@ -45,6 +45,12 @@ __device__ __forceinline__ uint32_t state_poll(const uint32_t* p) {
 }
 __device__ __forceinline__ void acquire_fence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ bool state_cas(uint32_t* p, uint32_t expected, uint32_t desired) {
     uint32_t old;
     asm volatile("atom.acq_rel.gpu.global.cas.b32 %0, [%1], %2, %3;"

@@ -51,6 +51,7 @@ struct SvPending {
     uint32_t rel[5];
     uint32_t n;
     unsigned long long pub;  // ticket whose hand-off flag is due (0 = none)
+    uint32_t pubw;           // its continuation word (slot | release-as-DELMOD << 31)
 };
 
 struct OpShared {
@@ -72,6 +73,8 @@ struct OpShared {
     unsigned long long op_next;    // its op index
     unsigned long long off_next;   // its out_pool offset
     unsigned long long dbg_ts;
+    uint32_t contw;                // served delete: continuation slot | kDelMod bit 31
+    uint32_t next_w;               // delete server: pre-observed state word of the next refill
     SvPending pd;
 };
 
@@ -258,9 +261,9 @@ struct HeapCta {
     // Queue slot line of ticket t: word 0 = hand-off flag (t<<1 granted,
     // t<<1|1 served by a combiner), word 1 = request word (t<<1|1 when the
     // waiter is a combinable insert), words 2-3 = its op index, words 4-9 =
-    // the combiner's response (insert: rank, target slot, root sequence;
-    // delete: continuation slot, its release state), word 11 = request
-    // word of a servable delete (t<<1|1).
+    // the combiner's response to an insert (rank, target slot, root
+    // sequence); word 11 = request word of a servable delete (t<<1|1), whose
+    // delete server writes words 0-1 at once: flag | continuation word << 32.
     __device__ __forceinline__ uint32_t* qline(unsigned long long t) const {
         return hv.root_flags + (t % kRootQueue) * kRootFlagStride;
     }
@@ -277,8 +280,17 @@ struct HeapCta {
         const uint32_t granted = (uint32_t)t << 1;
         uint32_t v;
         if (del_req) {
+            // words 0-1 in one load: a delete server's hand-off puts the
+            // continuation word (serve_deletes) next to the flag
             QuickBackoff b;
-            while (((v = state_load(f)) & ~1u) != granted) { b.pause(); BH_WAIT_NOTE(__LINE__); }
+            unsigned long long vv;
+            while ((((uint32_t)(vv = ld_acquire_u64(reinterpret_cast<const unsigned long long*>(f)))) & ~1u) !=
+                   granted) {
+                b.pause();
+                BH_WAIT_NOTE(__LINE__);
+            }
+            v = (uint32_t)vv;
+            sh->contw = (uint32_t)(vv >> 32);
         } else {
             Backoff b;
             while (((v = state_load(f)) & ~1u) != granted) { b.pause(); BH_WAIT_NOTE(__LINE__); }
@@ -1197,10 +1209,23 @@ struct HeapCta {
 
     // refill_root_from(last), claim + copy + blank + release, by threads
     // [base, base + nthr) with barrier `bar`.  The refill batch lands in dst.
-    __device__ void refill_last(unsigned long long last, Key* dst, uint32_t base, uint32_t nthr, uint32_t bar) {
+    // `pre`: a state word of `last` observed (acquire) earlier by this CTA;
+    // a claim from it skips the first poll (the CAS fails if it changed).
+    __device__ void refill_last(unsigned long long last, Key* dst, uint32_t base, uint32_t nthr, uint32_t bar,
+                                uint32_t pre = 0xFFFFFFFFu) {
         const uint32_t gt = threadIdx.x - base;
         for (;;) {
-            if (gt == 0) lane_poll_last(last);
+            if (gt == 0) {
+                const uint32_t ps = sget(pre);
+                if (ps == kAvail || ps == kDelMod) {
+                    sh->cw[2] = pre;
+                    sh->act = kTake;
+                    sh->lastrel = kAvail;
+                } else {
+                    lane_poll_last(last);
+                }
+                pre = 0xFFFFFFFFu;
+            }
             grp_sync(bar, nthr);
             const uint32_t act = sh->act;
             uint32_t ok = 0;
@@ -1288,7 +1313,8 @@ struct HeapCta {
         }
         if (pd.pub) {
             if (!fenced) __threadfence();
-            state_store_relaxed(qline(pd.pub), ((uint32_t)pd.pub << 1) | 1u);
+            const unsigned long long w = ((unsigned long long)pd.pubw << 32) | (((uint32_t)pd.pub << 1) | 1u);
+            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(qline(pd.pub)), "l"(w) : "memory");
         }
         pd.n = 0;
         pd.pub = 0;
@@ -1324,7 +1350,7 @@ struct HeapCta {
     //   r3     new hi1 || next carried    (halves of merge(carried, H1))
     __device__ unsigned long long serve_one(unsigned long long opi, unsigned long long off, unsigned long long seq,
                                             unsigned long long nodes, unsigned long long t, int& n1, int& n2,
-                                            int& n3, int& cbuf, uint32_t& crel) {
+                                            int& n3, int& cbuf, uint32_t& crel, uint32_t pre_w) {
         const unsigned long long ts0 = now();
         Key* out = static_cast<Key*>(rv.out_pool) + off;
         if (threadIdx.x >= kHalfT) {  // the result: the root's k keys (B group: no fences follow)
@@ -1383,11 +1409,14 @@ struct HeapCta {
                 const bool more = nodes - 1 >= kServeMin && waiting_delete(t + 1, nop);
                 sh->serve = more;
                 sh->op_next = nop;
-                if (more) sh->off_next = rv.ops[nop].offset;
+                if (more) {
+                    sh->off_next = rv.ops[nop].offset;
+                    sh->next_w = state_load(st(slot_for_rank(nodes - 1)));  // the next op's refill
+                }
             }
         } else if (threadIdx.x < kHalfT) {
             // released here, before the server waits on any claim (below)
-            refill_last(last, buf(rf), kRefBase, kHalfT - kRefBase, 1);
+            refill_last(last, buf(rf), kRefBase, kHalfT - kRefBase, 1, pre_w);
             if (prof && threadIdx.x == kRefBase) atomicAdd(&hv.prof[pfSvA], now() - ts0);
         } else {
             // both halves of merge(L, R): H0 and the lo child's new batch,
@@ -1396,8 +1425,16 @@ struct HeapCta {
             // last.  The refill beside it never waits while holding the last
             // node, so nothing but nodes 1-3 is held across this wait.
             if (mc0) {
-                cta_merge_half<Key, K, T, false, false>(L, R, buf(h0), threadIdx.x - kHalfT, kHalfT);
-                cta_merge_half<Key, K, T, true, false>(L, R, buf(nlo), threadIdx.x - kHalfT, kHalfT);
+                constexpr int kPB = 2 * HalfShape<K, T>::P;  // two halves on one group
+                constexpr uint32_t kTB = K / kPB;
+                if constexpr (2 * kTB == kHalfT) {
+                    const uint32_t bt = threadIdx.x - kHalfT;
+                    if (bt < kTB) cta_merge_half_p<Key, K, kPB, false, false>(L, R, buf(h0), bt, kTB);
+                    else cta_merge_half_p<Key, K, kPB, true, false>(L, R, buf(nlo), bt - kTB, kTB);
+                } else {
+                    cta_merge_half<Key, K, T, false, false>(L, R, buf(h0), threadIdx.x - kHalfT, kHalfT);
+                    cta_merge_half<Key, K, T, true, false>(L, R, buf(nlo), threadIdx.x - kHalfT, kHalfT);
+                }
             }
             if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvB], now() - ts0);
             const unsigned long long tc = now();
@@ -1535,6 +1572,7 @@ struct HeapCta {
         acquire_children(1, buf(n2), buf(n3));
         const uint32_t rel2 = sh->lrel, rel3 = sh->rrel;
         unsigned long long t = sh->root_tk, op = opi, served = 0, off = rv.ops[opi].offset;
+        uint32_t pre_w = 0xFFFFFFFFu;
         int cbuf = -1;
         uint32_t crel = kAvail;
         unsigned long long cont = 0;
@@ -1542,26 +1580,26 @@ struct HeapCta {
             sh->pd.n = 0;
             sh->pd.pub = 0;
         }
+
         for (;;) {
-            cont = serve_one(op, off, seq, nodes, t, n1, n2, n3, cbuf, crel);
+            cont = serve_one(op, off, seq, nodes, t, n1, n2, n3, cbuf, crel, pre_w);
             const unsigned long long tn = now();
             ++seq;
             --nodes;
             const bool more = sh->serve != 0;
             const unsigned long long nop = sh->op_next;
             const unsigned long long noff = sh->off_next;
+            pre_w = sh->next_w;  // the next op's refill word, observed in this op
             __syncthreads();  // everyone has read sh->serve / op_next
             if (!more) break;
             // the waiter of ticket t+1 takes this op's continuation (its
             // carried batch is in mbox(t+1)); its own op is served next.  The
             // flag goes out with the next op's flush.
             if (threadIdx.x == kPubLane) {
-                unsigned long long* f = reinterpret_cast<unsigned long long*>(qline(t + 1));
-                st_cg_u64(f + 2, cont);
-                st_cg_u64(f + 3, crel);
                 atomicAdd(&hdr->deleters, 1ull);  // op t+1 is in the delete phase
+                sh->pd.pub = t + 1;
+                sh->pd.pubw = (uint32_t)cont | (crel == kDelMod ? 0x80000000u : 0u);
             }
-            if (threadIdx.x == kPubLane) sh->pd.pub = t + 1;
             op = nop;
             off = noff;
             ++t;
@@ -1626,9 +1664,8 @@ struct HeapCta {
             // a delete server ran this op's top levels and wrote its result;
             // this CTA runs the continuation of the op served before it
             const unsigned long long tk = sh->root_tk;
-            const unsigned long long* f = reinterpret_cast<const unsigned long long*>(qline(tk));
-            const unsigned long long cont = ld_cg_u64(f + 2);  // words 4-5
-            const uint32_t crel = (uint32_t)(ld_cg_u64(f + 3) & 0xFFFFFFFFu);  // word 6
+            const unsigned long long cont = sh->contw & 0x7FFFFFFFu;
+            const uint32_t crel = (sh->contw >> 31) ? kDelMod : kAvail;
             if (cont) {
                 // the carried batch travels while the node's children are claimed
                 cta_load_async<Key, T>(buf(0), mbox(tk), K);

@@ -125,4 +125,20 @@ __device__ __forceinline__ void cta_merge_half(const Key* __restrict__ A, const 
     }
 }
 
+// cta_merge_half with an explicit window P (K / P threads cover a half);
+// the delete server runs both halves of a sibling merge side by side on one
+// thread group with it.
+template <typename Key, int K, int P, bool Second, bool Global>
+__device__ __forceinline__ void cta_merge_half_p(const Key* __restrict__ A, const Key* __restrict__ B,
+                                                 Key* __restrict__ out, uint32_t tid, uint32_t nthr) {
+    for (uint32_t t0 = tid * P; t0 < (uint32_t)K; t0 += nthr * P) {
+        const uint32_t d0 = (Second ? (uint32_t)K : 0u) + t0;
+        const uint32_t i = merge_split<Key, K>(A, B, d0, K, K);
+        Key run[P];
+        merge_window<Key, P>(A, i, K, B, d0 - i, K, run);
+        if constexpr (Global) store_run_cg<Key, P>(out + t0, run);
+        else store_run<Key, P>(out + t0, run);
+    }
+}
+
 }  // namespace bh
