@@ -21,7 +21,10 @@
 //     that saw the release); both children are claimed by two lanes at once;
 //   * the root is a FIFO array queue lock whose holder, when it is a BU
 //     full-batch insert, also runs the root phase of the BU full-batch
-//     inserts queued behind it (serve_inserts: insert combining);
+//     inserts queued behind it (serve_inserts: insert combining), and when
+//     it is a BU delete, runs levels 0-1 of the deletes queued behind it from
+//     shared memory and hands each one's lower heapify to the next waiter
+//     (serve_deletes: delete serving);
 //   * heapify_down's two-phase level schedule: the node is released right
 //     after the first-half merges that decide its batch; the carried and lo
 //     batches are finished afterwards while the other half of the CTA claims
