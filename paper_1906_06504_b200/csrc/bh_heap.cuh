@@ -75,7 +75,6 @@ struct OpShared {
     uint32_t serve;                // delete server: next ticket is a waiting delete
     unsigned long long op_next;    // its op index
     unsigned long long off_next;   // its out_pool offset
-    unsigned long long dbg_ts;
     uint32_t contw;                // served delete: continuation slot | kDelMod bit 31
     uint32_t next_w;               // delete server: pre-observed state word of the next refill
     SvPending pd;
@@ -120,10 +119,7 @@ enum ProfIdx {
     pfSvR2,     //   lo + H1 merges
     pfSvR3,     //   level-1 merges, lo2 write and release
     pfSvNext,   //   next-waiter check and continuation hand-off
-    pfSvR1a,    //   r1: leader's merge half done (from r1 start)
-    pfSvR1b,    //   r1: second group's merge half done
-    pfSvR2a,    //   r2: leader's merge half done (from r2 start)
-    pfSvR2b,    //   r2: second group's merge half done
+    pfSvClaim,  //   level-2 claim (after H0 || lo0)
     kNumProf
 };
 
@@ -1399,15 +1395,13 @@ struct HeapCta {
         const unsigned long long hi1 = hi_left ? 2 : 3;
         const unsigned long long c2l = 2 * hi1, c2r = 2 * hi1 + 1;
         const unsigned long long last = slot_for_rank(nodes);
-        // refill (claim, copy, blank; released with the next op's flush)
-        // || H0, the claim of hi1's children, lo0
-        // warps below kRefBase stay out of the refill group: the leader's bookkeeping
-        // and kPubLane's flush + next-waiter lookup run beside it
+        // split: refill (claim, copy, blank, release the last node) ||
+        // H0 and lo0, then the claim of hi1's children.  Warps below kRefBase
+        // stay out of both groups: the leader's bookkeeping and kPubLane's
+        // flush of the previous op + next-waiter lookup run beside them.
         if (threadIdx.x < kRefBase) {
             if (threadIdx.x == kPubLane) {
-#ifndef BH_EXP_LATEFLUSH
                 sv_flush(sh->pd);
-#endif
                 unsigned long long nop = 0;
                 const bool more = nodes - 1 >= kServeMin && waiting_delete(t + 1, nop);
                 sh->serve = more;
@@ -1442,16 +1436,11 @@ struct HeapCta {
             if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvB], now() - ts0);
             const unsigned long long tc = now();
             acquire_children(hi1, buf(l2), buf(r2), kHalfT, kHalfT, 2);
-            if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvR1b], now() - tc);
+            if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvClaim], now() - tc);
         }
-        if (prof && threadIdx.x == T - 1) sh->dbg_ts = seq;
         __syncthreads();
-        if (prof && leader() && sh->dbg_ts != seq) atomicAdd(&hv.prof[pfSvR2a], 1ull);
         const unsigned long long ts1 = now();
         pf_add(pfSvSplit, ts1 - ts0);
-#ifdef BH_EXP_LATEFLUSH
-        if (threadIdx.x == kPubLane) sv_flush(sh->pd);
-#endif
         const bool handoff = sh->serve != 0;
         const Key* RF = buf(rf);
 

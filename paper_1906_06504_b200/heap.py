@@ -280,7 +280,7 @@ class GeneralizedHeap:
                       "rs_fill", "lv_acq", "lv_load", "lv_merge", "lv_rel", "served",
                       "serve_holds", "bu_parent", "bu_retake", "bu_levels", "split_a", "split_b",
                       "del_served", "del_serve_holds", "sv_split", "sv_a", "sv_b", "sv_r1", "sv_r2",
-                      "sv_r3", "sv_next", "sv_r1a", "sv_r1b", "sv_r2a", "sv_r2b")
+                      "sv_r3", "sv_next", "sv_claim")
 
     def profile(self, reset: bool = True) -> dict:
         """SM-cycle profile of a BH_FLAG_PROFILE heap (see bh_profile)."""

@@ -71,7 +71,7 @@ for k in a.k:
                 print(f"   delete root split: refill half {us(p['split_a'], d):.2f} us, children half {us(p['split_b'], d):.2f} us", flush=True)
                 sv = max(p['del_served'] + p['del_serve_holds'], 1)
                 print(f"   delete serving: served {p['del_served']} in {p['del_serve_holds']} holds | per op us: "
-                      f"split {us(p['sv_split'], sv):.2f} (refill {us(p['sv_a'], sv):.2f}; H0+lo0 {us(p['sv_b'], sv):.2f} then claims {us(p['sv_r1b'], sv):.2f}) "
+                      f"split {us(p['sv_split'], sv):.2f} (refill {us(p['sv_a'], sv):.2f}; H0+lo0 {us(p['sv_b'], sv):.2f} then claims {us(p['sv_claim'], sv):.2f}) "
                       f"r1 {us(p['sv_r1'], sv):.2f} "
-                      f"r2 {us(p['sv_r2'], sv):.2f} r3 {us(p['sv_r3'], sv):.2f} next {us(p['sv_next'], sv):.2f} misaligned {p['sv_r2a']}", flush=True)
+                      f"r2 {us(p['sv_r2'], sv):.2f} r3 {us(p['sv_r3'], sv):.2f} next {us(p['sv_next'], sv):.2f}", flush=True)
             heap.close()
