@@ -274,6 +274,9 @@ struct HeapCta {
         uint32_t* f = qline(t);
         if (combinable || del_req) {
             st_cg_u64(reinterpret_cast<unsigned long long*>(f + 2), cur_op);
+            // a delete server serves only ops of its own launch (its ops,
+            // out_pool and status arrays): words 12-13 name the launch
+            if (del_req) st_cg_u64(reinterpret_cast<unsigned long long*>(f + 12), (unsigned long long)rv.ticket);
             state_store_release(f + (del_req ? 11 : 1), ((uint32_t)t << 1) | 1u);
         }
         const uint32_t granted = (uint32_t)t << 1;
@@ -1290,6 +1293,8 @@ struct HeapCta {
     __device__ bool waiting_delete(unsigned long long t, unsigned long long& op) {
         uint32_t* f = qline(t);
         if (state_load(f + 11) != (((uint32_t)t << 1) | 1u)) return false;
+        if (ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 12)) != (unsigned long long)rv.ticket)
+            return false;  // a delete of another launch: granted normally
         op = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 2));
         return true;
     }

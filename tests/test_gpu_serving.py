@@ -90,3 +90,44 @@ def test_serving_with_interleaved_inserts_conserves_keys():
     out = [r.out[o["offset"]:o["offset"] + r.lens[i]] for i, o in enumerate(ops) if o["kind"] == 1]
     got = np.sort(np.concatenate(out + [heap.collect_resident()]).astype(np.uint64))
     assert np.array_equal(got, np.sort(keys[:n + n_ins * k]))
+
+
+def test_serving_stays_within_its_launch():
+    """Two delete launches on two streams share the root queue: a server
+    must serve only ops of its own launch (their ops, out_pool and status
+    arrays).  Ordered by their delete sequence, the two launches' batches
+    together are the sorted prefix of the heap."""
+    import torch
+
+    k, n, m = 256, 1 << 19, 600
+    keys = O.generate_keys(n, 21).astype(np.uint64)
+    heap = GeneralizedHeap(Variant.BU, k, n // k + 64, key_bits=32)
+    assert np.all(heap.run_ops(phase_ops(0, n, k), keys.astype(np.uint32), 0).status == 0)
+    dev = torch.device("cuda", 0)
+    runs = []
+    for _ in range(2):
+        ops = torch.from_numpy(phase_ops(1, m * k, k).view(np.uint8)).to(dev)
+        runs.append(dict(ops=ops, out=torch.zeros(m * k, dtype=torch.int32, device=dev),
+                         st=torch.full((m,), 99, dtype=torch.int32, device=dev),
+                         ln=torch.zeros(m, dtype=torch.int32, device=dev),
+                         sq=torch.zeros(m, dtype=torch.int64, device=dev), stream=torch.cuda.Stream(dev)))
+    torch.cuda.synchronize(dev)
+    ctas = max(heap.max_ctas // 2, 2)
+    for r in runs:
+        heap.run_ops_ptr(r["ops"].data_ptr(), m, 0, r["out"].data_ptr(), r["st"].data_ptr(), r["ln"].data_ptr(),
+                         r["sq"].data_ptr(), ctas=ctas, stream=r["stream"].cuda_stream)
+    torch.cuda.synchronize(dev)
+    seqs, batches = [], []
+    for r in runs:
+        st = r["st"].cpu().numpy()
+        assert np.all(st == 0), np.unique(st)
+        assert np.all(r["ln"].cpu().numpy() == k)
+        out = r["out"].cpu().numpy().view(np.uint32).reshape(m, k).astype(np.uint64)
+        seqs.append(r["sq"].cpu().numpy())
+        batches.append(out)
+    seq = np.concatenate(seqs)
+    allb = np.concatenate(batches)[np.argsort(seq, kind="stable")]
+    assert np.array_equal(np.sort(seq), np.arange(2 * m))
+    assert np.array_equal(allb.reshape(-1), np.sort(keys)[:2 * m * k])
+    rep = heap.check_invariants()
+    assert rep.ok, rep.detail
