@@ -275,8 +275,9 @@ struct HeapCta {
         if (combinable || del_req) {
             st_cg_u64(reinterpret_cast<unsigned long long*>(f + 2), cur_op);
             // a delete server serves only ops of its own launch (its ops,
-            // out_pool and status arrays): words 12-13 name the launch
-            if (del_req) st_cg_u64(reinterpret_cast<unsigned long long*>(f + 12), (unsigned long long)rv.ticket);
+            // out_pool and status arrays), an insert combiner of a recorded
+            // heap too (it logs the waiter's events): words 12-13 name the launch
+            st_cg_u64(reinterpret_cast<unsigned long long*>(f + 12), (unsigned long long)rv.ticket);
             state_store_release(f + (del_req ? 11 : 1), ((uint32_t)t << 1) | 1u);
         }
         const uint32_t granted = (uint32_t)t << 1;
@@ -330,6 +331,8 @@ struct HeapCta {
         unsigned long long op = 0;
         if (ok) {
             ok = state_load(f + 1) == (((uint32_t)t << 1) | 1u);
+            if (ok && record)
+                ok = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 12)) == (unsigned long long)rv.ticket;
             if (ok) op = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 2));
         }
         const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
