@@ -114,7 +114,7 @@ struct bh_heap {
     uint32_t* d_root_flags = nullptr;
     Header* d_hdr = nullptr;
     void* d_partial = nullptr;
-    void* d_mailbox = nullptr;  // BU: carried batches handed to served deletes
+    void* d_mailbox = nullptr;  // carried batches handed to served deletes
     unsigned long long* d_counters = nullptr;
     unsigned long long* d_prof = nullptr;
     unsigned long long* d_tickets = nullptr;  // ring of bulk tickets
@@ -393,8 +393,7 @@ int bh_create(bh_heap** out, int variant, uint32_t k, uint32_t max_nodes, uint32
     if ((e = cudaMalloc(&h->d_hdr, sizeof(Header))) != cudaSuccess) return cleanup(cuda_fail(e, "hdr"));
     if ((e = cudaMalloc(&h->d_partial, std::max<size_t>((size_t)k * h->key_size, 16))) != cudaSuccess)
         return cleanup(cuda_fail(e, "partial"));
-    if (variant == BH_BU &&
-        (e = cudaMalloc(&h->d_mailbox, (size_t)kRootQueue * k * h->key_size)) != cudaSuccess)
+    if ((e = cudaMalloc(&h->d_mailbox, (size_t)kRootQueue * k * h->key_size)) != cudaSuccess)
         return cleanup(cuda_fail(e, "mailbox"));
     if ((e = cudaMalloc(&h->d_counters, kNumCounters * 8)) != cudaSuccess)
         return cleanup(cuda_fail(e, "counters"));

@@ -1259,8 +1259,8 @@ struct HeapCta {
     }
 
     // ================================================== delete serving ==
-    // Flat combining of deletes in the root queue lock (BU heaps, delete
-    // phase).  A delete holding the root with deletes queued behind it keeps
+    // Flat combining of deletes in the root queue lock (TD and BU heaps; BU
+    // deletes pass the phase gate first, as their own root step would).  A delete holding the root with deletes queued behind it keeps
     // the root and nodes 2-3 (claimed, in shared memory) and runs, for its own
     // op and then each queued delete in ticket order, the reference's
     // delete_min through levels 0 and 1: root result, refill from the last
@@ -1596,7 +1596,7 @@ struct HeapCta {
             // carried batch is in mbox(t+1)); its own op is served next.  The
             // flag goes out with the next op's flush.
             if (threadIdx.x == kPubLane) {
-                atomicAdd(&hdr->deleters, 1ull);  // op t+1 is in the delete phase
+                if (hv.variant == BH_BU) atomicAdd(&hdr->deleters, 1ull);  // op t+1 is in the delete phase
                 sh->pd.pub = t + 1;
                 sh->pd.pubw = (uint32_t)cont | (crel == kDelMod ? 0x80000000u : 0u);
             }
@@ -1625,7 +1625,7 @@ struct HeapCta {
         pf_add(pfDelServed, served);
         pf_add(pfDelServeHolds, served ? 1 : 0);
         if (cont) heapify_down(cbuf, 0, false, cont, crel);
-        if (leader()) gate_leave(false);
+        if (hv.variant == BH_BU && leader()) gate_leave(false);
     }
 
     __device__ void do_delete(unsigned long long opi, const bh_op& o) {
@@ -1654,7 +1654,9 @@ struct HeapCta {
                 }
                 rec(kEvAcq, 1);
             } else {
-                root_lock();
+                // TD: no phase gate; the request lets a delete server run it
+                const bool can_post = T >= 128 && !record && (hv.flags & kDbgNoDelServe) == 0;
+                if (root_lock(true, false, can_post)) gated = 2;
             }
             sh->owned = gated;
         }
@@ -1674,7 +1676,7 @@ struct HeapCta {
                 __syncthreads();
                 heapify_down(0, t1, true, cont, crel);
             }
-            if (leader()) gate_leave(false);
+            if (hv.variant == BH_BU && leader()) gate_leave(false);
             return;
         }
         const bool gated = sh->owned != 0;
@@ -1684,6 +1686,14 @@ struct HeapCta {
             sh->nodes = ld_cg_u64(&hdr->node_count);
             sh->plen = ld_cg_u64(&hdr->partial_len);
             sh->seq = ld_cg_u64(&hdr->delete_count);
+            // peek (relaxed, same round trip) at the next ticket's serve
+            // request; TD heaps start serving only for a run of deletes (two
+            // queued), short runs between inserts do not pay for it
+            const unsigned long long t1q = sh->root_tk + 1;
+            bool peek = __ldcg(qline(t1q) + 11) == ((((uint32_t)t1q) << 1) | 1u);
+            if (hv.variant == BH_TD)
+                peek = peek && __ldcg(qline(t1q + 1) + 11) == ((((uint32_t)t1q + 1u) << 1) | 1u);
+            sh->serve = peek;
         }
         cta_load<Key, T>(cur_s, node(1), K);
         __syncthreads();
@@ -1727,8 +1737,9 @@ struct HeapCta {
 
         // delete serving: with waiting deletes queued behind, this CTA keeps
         // the root and runs their top levels too
-        if (T >= 128 && gated && plen == 0 && nodes >= kServeMin && !record && (hv.flags & kDbgNoDelServe) == 0) {
-            if (leader()) {
+        if (T >= 128 && (gated || hv.variant == BH_TD) && plen == 0 && nodes >= kServeMin && !record &&
+            (hv.flags & kDbgNoDelServe) == 0) {
+            if (leader() && sh->serve) {
                 unsigned long long nop = 0;
                 sh->serve = waiting_delete(sh->root_tk + 1, nop);
             }

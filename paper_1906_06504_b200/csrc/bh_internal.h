@@ -92,7 +92,7 @@ struct HeapView {
     uint32_t* root_flags;    // kRootQueue * kRootFlagStride
     Header* hdr;
     void* partial;           // k keys
-    void* mailbox;           // kRootQueue * k keys: carried batches of served deletes (BU)
+    void* mailbox;           // kRootQueue * k keys: carried batches of served deletes
     unsigned long long* counters;
     unsigned long long* prof;  // non-null on BH_FLAG_PROFILE handles
     unsigned long long slot_count;

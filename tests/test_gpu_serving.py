@@ -1,4 +1,4 @@
-"""Delete serving (bh_heap.cuh serve_deletes): a BU delete holding the root
+"""Delete serving (bh_heap.cuh serve_deletes): a delete holding the root
 with deletes queued behind it runs their levels 0-1 from shared memory and
 hands each continuation to the next waiter.  Compared with the one-root-hold-
 per-delete path (kDbgNoDelServe): the same deleted batches in the same order
@@ -24,13 +24,14 @@ def _deleted(heap, n_ops, k):
     return np.concatenate([out[i, :lens[i]] for i in range(n_ops)]).astype(np.uint64)
 
 
+@pytest.mark.parametrize("variant", [Variant.BU, Variant.TD])
 @pytest.mark.parametrize("k", [256, 1024, 2048])
-def test_serving_engages_and_drains_sorted(k):
+def test_serving_engages_and_drains_sorted(k, variant):
     n = 1 << 20
     keys = O.generate_keys(n, 11)
     served = {}
     for flags in (0, NO_DEL_SERVE):
-        heap = GeneralizedHeap(Variant.BU, k, n // k + 64, key_bits=32, profile=True, debug_flags=flags)
+        heap = GeneralizedHeap(variant, k, n // k + 64, key_bits=32, profile=True, debug_flags=flags)
         assert np.all(heap.run_ops(phase_ops(0, n, k), keys.astype(np.uint32), 0).status == 0)
         heap.profile(reset=True)
         got = _deleted(heap, n // k, k)
@@ -42,11 +43,12 @@ def test_serving_engages_and_drains_sorted(k):
     assert served[NO_DEL_SERVE] == 0
 
 
+@pytest.mark.parametrize("variant", [Variant.BU, Variant.TD])
 @pytest.mark.parametrize("k", [256, 1024])
-def test_serving_partial_phase_leaves_a_valid_heap(k):
+def test_serving_partial_phase_leaves_a_valid_heap(k, variant):
     n = (1 << 19) + 5 * k
     keys = O.generate_keys(n, 12).astype(np.uint64)
-    heap = GeneralizedHeap(Variant.BU, k, 2 * (n // k) + 64, key_bits=32)
+    heap = GeneralizedHeap(variant, k, 2 * (n // k) + 64, key_bits=32)
     assert np.all(heap.run_ops(phase_ops(0, n, k), keys.astype(np.uint32), 0).status == 0)
     m = (n // k) // 2
     srt = np.sort(keys)
@@ -62,12 +64,13 @@ def test_serving_partial_phase_leaves_a_valid_heap(k):
     assert np.array_equal(_deleted(heap, rest.size // k, k), rest)
 
 
-def test_serving_with_interleaved_inserts_conserves_keys():
+@pytest.mark.parametrize("variant", [Variant.BU, Variant.TD])
+def test_serving_with_interleaved_inserts_conserves_keys(variant):
     """Delete runs broken by inserts (BU phase gate included): servers stop at an insert in the queue;
     every key inserted comes out once, invariants hold at quiescence."""
     k, n = 1024, 1 << 19
     keys = O.generate_keys(2 * n, 14).astype(np.uint64)
-    heap = GeneralizedHeap(Variant.BU, k, 2 * (2 * n // k) + 64, key_bits=32)
+    heap = GeneralizedHeap(variant, k, 2 * (2 * n // k) + 64, key_bits=32)
     assert np.all(heap.run_ops(phase_ops(0, n, k), keys[:n].astype(np.uint32), 0).status == 0)
     # 3 deletes, 1 insert, repeated
     n_ins = (n // k) // 2

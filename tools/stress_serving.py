@@ -32,7 +32,8 @@ for run in range(a.runs):
     keys = O.generate_keys(n, 1000 + run).astype(np.uint64)
     extra = int(rng.integers(0, 3)) * (n // k // 4) * k
     more = O.generate_keys(max(extra, 1), 5000 + run).astype(np.uint64)[:extra]
-    heap = GeneralizedHeap(Variant.BU, k, 2 * ((n + extra) // k) + 64, key_bits=32)
+    variant = Variant.BU if rng.random() < 0.5 else Variant.TD
+    heap = GeneralizedHeap(variant, k, 2 * ((n + extra) // k) + 64, key_bits=32)
     ok = True
     r = heap.run_ops(phase_ops(0, n, k), keys.astype(np.uint32), 0, ctas=ctas)
     ok &= bool(np.all(r.status == 0))
@@ -69,7 +70,7 @@ for run in range(a.runs):
         ok &= bool(np.array_equal(seq_out, np.sort(keys)[:seq_out.size]))
     heap.close()
     fails += not ok
-    print(f"run {run:3d} k={k:4d} n={n:8d} extra={extra:7d} ctas={ctas:3d} del={n_del:5d} every={every:2d} "
+    print(f"run {run:3d} {variant.name} k={k:4d} n={n:8d} extra={extra:7d} ctas={ctas:3d} del={n_del:5d} every={every:2d} "
           f"{'ok' if ok else 'FAIL ' + rep.detail}", flush=True)
 print(f"{a.runs - fails}/{a.runs} ok in {time.time() - t0:.1f} s")
 sys.exit(1 if fails else 0)
