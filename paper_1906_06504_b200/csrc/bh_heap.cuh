@@ -51,10 +51,12 @@ namespace bh {
 // Releases a delete server has deferred to its next op (kPubLane only).
 struct SvPending {
     unsigned long long slot[5];
+    unsigned long long op[5];  // op each release belongs to (recorded heaps)
     uint32_t rel[5];
     uint32_t n;
     unsigned long long pub;  // ticket whose hand-off flag is due (0 = none)
     uint32_t pubw;           // its continuation word (slot | release-as-DELMOD << 31)
+    unsigned long long pubop;  // op whose continuation it is (recorded heaps)
 };
 
 struct OpShared {
@@ -1302,9 +1304,12 @@ struct HeapCta {
         return true;
     }
 
-    __device__ __forceinline__ void pend(unsigned long long slot, uint32_t rel) {
+    // op = ~0: a release not logged (nodes 2-3 at the end of a hold: each
+    // served op logged its own spans of them)
+    __device__ __forceinline__ void pend(unsigned long long slot, uint32_t rel, unsigned long long op = 0) {
         if (threadIdx.x == kPubLane) {
             sh->pd.slot[sh->pd.n] = slot;
+            sh->pd.op[sh->pd.n] = op == ~0ull ? ~0ull : cur_op;
             sh->pd.rel[sh->pd.n] = rel;
             ++sh->pd.n;
         }
@@ -1313,7 +1318,10 @@ struct HeapCta {
     // kPubLane: the previous op's releases, one fence for all of them.
     __device__ void sv_flush(SvPending& pd) {
         bool fenced = false;
+        if (pd.pub && record)  // the op the woken CTA continues, for its events
+            st_cg_u64(reinterpret_cast<unsigned long long*>(qline(pd.pub) + 14), pd.pubop);
         for (uint32_t i = 0; i < pd.n; ++i) {
+            if (record && pd.op[i] != ~0ull) rec_for(pd.op[i], kEvRel, pd.slot[i]);
             if (!fenced) state_release(st(pd.slot[i]), kInUse, pd.rel[i]);
             else state_release_relaxed(st(pd.slot[i]), kInUse, pd.rel[i]);
             fenced = true;
@@ -1443,10 +1451,13 @@ struct HeapCta {
             }
             if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvB], now() - ts0);
             const unsigned long long tc = now();
-            acquire_children(hi1, buf(l2), buf(r2), kHalfT, kHalfT, 2);
+            if (!record) acquire_children(hi1, buf(l2), buf(r2), kHalfT, kHalfT, 2);
             if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvClaim], now() - tc);
         }
         __syncthreads();
+        // recorded heaps keep the reference's top-down lock order in their
+        // histories: the claim follows the refill's release
+        if (record) acquire_children(hi1, buf(l2), buf(r2));
         const unsigned long long ts1 = now();
         pf_add(pfSvSplit, ts1 - ts0);
         const bool handoff = sh->serve != 0;
@@ -1582,7 +1593,18 @@ struct HeapCta {
         }
 
         for (;;) {
+            cur_op = op;  // the lock events of this op's top levels are its own
+            if (record && served && leader()) {  // the first op holds 1-3 already
+                rec(kEvAcq, 1);
+                rec(kEvAcq, 2);
+                rec(kEvAcq, 3);
+            }
             cont = serve_one(op, off, seq, nodes, t, n1, n2, n3, cbuf, crel, pre_w);
+            if (record && leader()) {
+                rec(kEvRel, 2);
+                rec(kEvRel, 3);
+                rec(kEvRel, 1);
+            }
             const unsigned long long tn = now();
             ++seq;
             --nodes;
@@ -1599,6 +1621,7 @@ struct HeapCta {
                 if (hv.variant == BH_BU) atomicAdd(&hdr->deleters, 1ull);  // op t+1 is in the delete phase
                 sh->pd.pub = t + 1;
                 sh->pd.pubw = (uint32_t)cont | (crel == kDelMod ? 0x80000000u : 0u);
+                sh->pd.pubop = op;
             }
             op = nop;
             off = noff;
@@ -1615,7 +1638,7 @@ struct HeapCta {
             st_cg_u64(&hdr->delete_count, seq);
         }
         __syncthreads();
-        pend(2, rel2);
+        pend(2, rel2, ~0ull);
         if (threadIdx.x == kPubLane) {
             sv_flush(sh->pd);
             state_release_relaxed(st(3), kInUse, rel3);
@@ -1624,7 +1647,9 @@ struct HeapCta {
         }
         pf_add(pfDelServed, served);
         pf_add(pfDelServeHolds, served ? 1 : 0);
+        cur_op = op;  // the last op served: its continuation stays here
         if (cont) heapify_down(cbuf, 0, false, cont, crel);
+        rec(kEvRes, 0);
         if (hv.variant == BH_BU && leader()) gate_leave(false);
     }
 
@@ -1637,7 +1662,7 @@ struct HeapCta {
                 // BU phase gate: a delete that will heapify (>= 2 nodes) waits
                 // until no bottom-up climb is in flight.  The request lets a
                 // delete server ahead in the queue run this op (serve_deletes).
-                const bool can_post = T >= 128 && !record && (hv.flags & kDbgNoDelServe) == 0;
+                const bool can_post = T >= 128 && (hv.flags & kDbgNoDelServe) == 0;
                 for (;;) {
                     if (root_lock(false, false, can_post)) {
                         gated = 2;  // served: counted in the gate by the server
@@ -1652,10 +1677,10 @@ struct HeapCta {
                     root_unlock(false);
                     gate_wait(false);
                 }
-                rec(kEvAcq, 1);
+                if (gated != 2) rec(kEvAcq, 1);
             } else {
                 // TD: no phase gate; the request lets a delete server run it
-                const bool can_post = T >= 128 && !record && (hv.flags & kDbgNoDelServe) == 0;
+                const bool can_post = T >= 128 && (hv.flags & kDbgNoDelServe) == 0;
                 if (root_lock(true, false, can_post)) gated = 2;
             }
             sh->owned = gated;
@@ -1668,6 +1693,11 @@ struct HeapCta {
             const unsigned long long tk = sh->root_tk;
             const unsigned long long cont = sh->contw & 0x7FFFFFFFu;
             const uint32_t crel = (sh->contw >> 31) ? kDelMod : kAvail;
+            if (record) {  // its lock events and response are that op's
+                if (leader()) sh->op_next = ld_cg_u64(reinterpret_cast<const unsigned long long*>(qline(tk) + 14));
+                __syncthreads();
+                cur_op = sh->op_next;
+            }
             if (cont) {
                 // the carried batch travels while the node's children are claimed
                 cta_load_async<Key, T>(buf(0), mbox(tk), K);
@@ -1676,6 +1706,7 @@ struct HeapCta {
                 __syncthreads();
                 heapify_down(0, t1, true, cont, crel);
             }
+            rec(kEvRes, 0);
             if (hv.variant == BH_BU && leader()) gate_leave(false);
             return;
         }
@@ -1737,7 +1768,7 @@ struct HeapCta {
 
         // delete serving: with waiting deletes queued behind, this CTA keeps
         // the root and runs their top levels too
-        if (T >= 128 && (gated || hv.variant == BH_TD) && plen == 0 && nodes >= kServeMin && !record &&
+        if (T >= 128 && (gated || hv.variant == BH_TD) && plen == 0 && nodes >= kServeMin &&
             (hv.flags & kDbgNoDelServe) == 0) {
             if (leader() && sh->serve) {
                 unsigned long long nop = 0;
@@ -1781,7 +1812,9 @@ struct HeapCta {
         const unsigned long long ta = now();
         pf_add(pfRsHead, ta - t1);
         if (plen) cta_load<Key, T>(sp, partial, plen);
-        const bool split = T >= 64 && nodes >= 4;
+        // (recorded heaps keep the reference's order in their histories:
+        // children claimed after the refill released the last node)
+        const bool split = T >= 64 && nodes >= 4 && !record;
         if (split) {
             constexpr uint32_t kHalf = T / 2;
             if (threadIdx.x < kHalf) {

@@ -134,3 +134,49 @@ def test_serving_stays_within_its_launch():
     assert np.array_equal(allb.reshape(-1), np.sort(keys)[:2 * m * k])
     rep = heap.check_invariants()
     assert rep.ok, rep.detail
+
+
+@pytest.mark.parametrize("variant", [Variant.BU, Variant.TD])
+def test_served_deletes_recorded_history_is_linearizable(variant):
+    """Recorded heaps serve deletes too: each served op's root window and
+    its node 1-3 spans are logged inside the server's hold, its lower lock
+    events and response by the CTA that runs its continuation.  The history
+    passes the same checkers as unserved runs."""
+    from oracle import lincheck as LC
+    from test_gpu_bulk import _recorded_history
+
+    k = 256
+    rng = np.random.default_rng(31 + int(variant))
+    chunks, kinds, lens, offs = [], [], [], []
+    at = out_at = 0
+    plan = [0] * 200 + [1] * 100 + [int(x) for x in rng.integers(0, 2, size=60)]
+    for kind in plan:
+        if kind == 0:
+            chunks.append(rng.integers(0, 1 << 40, size=k, dtype=np.uint64))
+            kinds.append(0); lens.append(k); offs.append(at)
+            at += k
+        else:
+            kinds.append(1); lens.append(0); offs.append(out_at)
+            out_at += k
+    ops = make_ops(np.array(kinds, np.uint32), np.array(lens, np.uint32), np.array(offs, np.uint64))
+    pool = np.concatenate(chunks)
+    served = 0
+    for trial in range(4):
+        heap = GeneralizedHeap(variant, k, 600, record=True, profile=True)
+        r = heap.run_ops(ops, pool, out_at, ctas=12)  # the delete block queues up
+        assert set(np.unique(r.status).tolist()) <= {0, 3}
+        served += heap.profile()["del_served"]
+        hist = _recorded_history(heap, ops, r, pool)
+        assert LC.validate(hist) is None
+        ok, why = LC.check_mutual_exclusion(hist)
+        assert ok, why
+        ok, why = LC.check_lock_order(hist)
+        assert ok, why
+        res = LC.check_td(hist, k) if variant == Variant.TD else LC.check_bu(hist, k)
+        assert res.passed, res.detail
+        jit = LC.check_jit(hist, k)
+        assert jit.passed, jit.detail
+        rep = heap.check_invariants()
+        assert rep.ok, rep.detail
+        heap.close()
+    assert served > 0  # the history covered served deletes
