@@ -139,7 +139,9 @@ enum ProfIdx {
 #endif
 constexpr uint32_t kDbgWaitBase = 48;
 
-template <typename Key, int K, int T>
+// Rec: the kernel of BH_FLAG_RECORD heaps (event log); the other kernel
+// carries no recording code at all.
+template <typename Key, int K, int T, bool Rec>
 struct HeapCta {
     static constexpr Key kMaxKey = KeyLimits<Key>::kMax;
     static constexpr int kBufs = 10;
@@ -159,7 +161,7 @@ struct HeapCta {
     unsigned long long cnt[kNumCounters];
     unsigned long long cur_op;
     bool elide;
-    bool record;
+    static constexpr bool record = Rec;
     bool prof;
 
     __device__ __forceinline__ HeapCta(const HeapView& h, const RunView& r, unsigned char* smem,
@@ -173,7 +175,6 @@ struct HeapCta {
 #pragma unroll
         for (int i = 0; i < kNumCounters; ++i) cnt[i] = 0;
         elide = (h.flags & BH_FLAG_ELIDE_MERGES) != 0;
-        record = (h.flags & BH_FLAG_RECORD) != 0;
         prof = h.prof != nullptr;
     }
 
@@ -2035,11 +2036,11 @@ struct HeapCta {
     }
 };
 
-template <typename Key, int K, int T>
+template <typename Key, int K, int T, bool Rec>
 __global__ void __launch_bounds__(T, (512 / T > 0 ? 512 / T : 1)) heap_ops_kernel(HeapView hv, RunView rv) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ OpShared sh;
-    HeapCta<Key, K, T> cta(hv, rv, smem_raw, &sh);
+    HeapCta<Key, K, T, Rec> cta(hv, rv, smem_raw, &sh);
     cta.run();
 }
 

@@ -95,10 +95,10 @@ __global__ void gather_kernel(HeapView hv, unsigned long long nodes, Key* out) {
     }
 }
 
-template <typename Key, int K>
-int launch_ops_k(const HeapView& hv, const RunView& rv, uint32_t ctas, cudaStream_t stream) {
+template <typename Key, int K, bool Rec>
+int launch_ops_kr(const HeapView& hv, const RunView& rv, uint32_t ctas, cudaStream_t stream) {
     using Cfg = KernelCfg<Key, K>;
-    auto kern = heap_ops_kernel<Key, K, Cfg::kThreads>;
+    auto kern = heap_ops_kernel<Key, K, Cfg::kThreads, Rec>;
     static bool attr_set = false;  // dynamic + static smem may pass 48 KB
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
@@ -109,10 +109,17 @@ int launch_ops_k(const HeapView& hv, const RunView& rv, uint32_t ctas, cudaStrea
     return note_cuda(cudaGetLastError());
 }
 
+// BH_FLAG_RECORD heaps run the kernel with the event log compiled in.
+template <typename Key, int K>
+int launch_ops_k(const HeapView& hv, const RunView& rv, uint32_t ctas, cudaStream_t stream) {
+    if (hv.flags & BH_FLAG_RECORD) return launch_ops_kr<Key, K, true>(hv, rv, ctas, stream);
+    return launch_ops_kr<Key, K, false>(hv, rv, ctas, stream);
+}
+
 template <typename Key, int K>
 int kernel_info_k(KernelInfo* info) {
     using Cfg = KernelCfg<Key, K>;
-    auto kern = heap_ops_kernel<Key, K, Cfg::kThreads>;
+    auto kern = heap_ops_kernel<Key, K, Cfg::kThreads, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (e != cudaSuccess) return note_cuda(e);
     int blocks = 0;
