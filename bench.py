@@ -288,6 +288,7 @@ def run_ours(a, rank: int, world: int, dist):
         h_seq = torch.empty(n_ops, dtype=torch.int64).pin_memory()
         e2e_times = []
         for i in range(2 + a.steps):
+            flush.fill_(3)  # L2 flushed between e2e steps too (outside the timed region)
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
