@@ -802,6 +802,25 @@ extern "C" __attribute__((visibility("default"))) int bh_debug_states(bh_heap* h
     return BH_OK;
 }
 
+// Debug: the raw heap header (2 x 128 bytes), on the aux stream.
+extern "C" __attribute__((visibility("default"))) int bh_debug_header(bh_heap* h, uint64_t* out, uint64_t words) {
+    if (!h || !out) return fail(BH_E_CONFIG, "null argument");
+    BH_CUDA(cudaSetDevice(h->device));
+    const uint64_t n = std::min<uint64_t>(words, sizeof(Header) / 8);
+    BH_CUDA(cudaMemcpyAsync(out, h->d_hdr, n * 8, cudaMemcpyDeviceToHost, h->aux));
+    BH_CUDA(cudaStreamSynchronize(h->aux));
+    return BH_OK;
+}
+
+// Debug: the first `bytes` of the delete-serving mailbox.
+extern "C" __attribute__((visibility("default"))) int bh_debug_mailbox(bh_heap* h, void* out, uint64_t bytes) {
+    if (!h || !out) return fail(BH_E_CONFIG, "null argument");
+    BH_CUDA(cudaSetDevice(h->device));
+    BH_CUDA(cudaMemcpyAsync(out, h->d_mailbox, bytes, cudaMemcpyDeviceToHost, h->aux));
+    BH_CUDA(cudaStreamSynchronize(h->aux));
+    return BH_OK;
+}
+
 int bh_sort_batches(uint32_t key_bits, uint32_t k, void* keys, const uint32_t* lens, uint64_t batches,
                     void* stream) {
     if (!valid_k(k) || (key_bits != 32 && key_bits != 64)) return fail(BH_E_CONFIG, "bad k or key_bits");

@@ -125,7 +125,7 @@ __device__ __forceinline__ void grp_sync(uint32_t id, uint32_t nthr) {
     if (id == 0)
         __syncthreads();
     else
-        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory");
+        asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory");
 }
 
 // Group versions of the node moves (thread `tid` of `nthr`).

@@ -669,7 +669,7 @@ struct HeapCta {
                 nd = t;
             }
         } else {
-            cta_merge_full<Key, K, T>(nd, bat, node(slot), tmp);
+            cta_merge_full_bt<Key, K, T>(nd, bat, node(slot), tmp);
             count(cMerges);
             Key* t = bat;
             bat = tmp;
@@ -954,7 +954,7 @@ struct HeapCta {
                     cta_store<Key, T>(node(parent), cu, K);
                     cta_store<Key, T>(node(cur), par, K);
                 } else {
-                    cta_merge_full<Key, K, T>(cu, par, node(parent), node(cur));
+                    cta_merge_full_bt<Key, K, T>(cu, par, node(parent), node(cur));
                     count(cMerges);
                 }
                 count(cVisits);
@@ -1069,7 +1069,7 @@ struct HeapCta {
                 count(cElided);
                 swap = true;  // C < P entirely: parent takes C, the slot takes P
             } else {
-                cta_merge_full<Key, K, T>(C, P, buf(ni), buf(si));
+                cta_merge_full_bt<Key, K, T>(C, P, buf(ni), buf(si));
                 count(cMerges);
             }
             if (!stop) count(cVisits);
@@ -1341,16 +1341,18 @@ struct HeapCta {
     template <bool S1, bool S2, bool G2 = false>
     __device__ __forceinline__ void two_halves(const Key* A1, const Key* B1, Key* o1, bool do1, const Key* A2,
                                                const Key* B2, Key* o2, bool do2) {
-        if constexpr (HalfShape<K, T>::kPair) {
-            constexpr uint32_t kT = HalfShape<K, T>::kThreads;
-            if (threadIdx.x < kT) {
-                if (do1) cta_merge_half<Key, K, T, S1, false>(A1, B1, o1, threadIdx.x, kT);
-            } else if (threadIdx.x < 2 * kT) {
-                if (do2) cta_merge_half<Key, K, T, S2, G2>(A2, B2, o2, threadIdx.x - kT, kT);
+        constexpr int kW = T / 32;
+        const uint32_t w = threadIdx.x >> 5;
+        if constexpr (kW >= 2) {
+            constexpr int kH = kW / 2;
+            if (w < (uint32_t)kH) {
+                if (do1) grp_merge_half<Key, K, kH, S1, false>(A1, B1, o1, w);
+            } else if (w < 2u * kH) {
+                if (do2) grp_merge_half<Key, K, kH, S2, G2>(A2, B2, o2, w - kH);
             }
         } else {
-            if (do1) cta_merge_half<Key, K, T, S1, false>(A1, B1, o1, threadIdx.x, T);
-            if (do2) cta_merge_half<Key, K, T, S2, G2>(A2, B2, o2, threadIdx.x, T);
+            if (do1) grp_merge_half<Key, K, 1, S1, false>(A1, B1, o1, 0);
+            if (do2) grp_merge_half<Key, K, 1, S2, G2>(A2, B2, o2, 0);
         }
     }
 
@@ -1439,16 +1441,11 @@ struct HeapCta {
             // last.  The refill beside it never waits while holding the last
             // node, so nothing but nodes 1-3 is held across this wait.
             if (mc0) {
-                constexpr int kPB = 2 * HalfShape<K, T>::P;  // two halves on one group
-                constexpr uint32_t kTB = K / kPB;
-                if constexpr (2 * kTB == kHalfT) {
-                    const uint32_t bt = threadIdx.x - kHalfT;
-                    if (bt < kTB) cta_merge_half_p<Key, K, kPB, false, false>(L, R, buf(h0), bt, kTB);
-                    else cta_merge_half_p<Key, K, kPB, true, false>(L, R, buf(nlo), bt - kTB, kTB);
-                } else {
-                    cta_merge_half<Key, K, T, false, false>(L, R, buf(h0), threadIdx.x - kHalfT, kHalfT);
-                    cta_merge_half<Key, K, T, true, false>(L, R, buf(nlo), threadIdx.x - kHalfT, kHalfT);
-                }
+                // two quarter groups side by side (T >= 128 here)
+                constexpr int kQ = T >= 128 ? T / 128 : 1;
+                const uint32_t bw = (threadIdx.x - kHalfT) >> 5;
+                if (bw < (uint32_t)kQ) grp_merge_half<Key, K, kQ, false, false>(L, R, buf(h0), bw);
+                else grp_merge_half<Key, K, kQ, true, false>(L, R, buf(nlo), bw - kQ);
             }
             if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvB], now() - ts0);
             const unsigned long long tc = now();
@@ -1957,7 +1954,7 @@ struct HeapCta {
             // ---- phase 1 ----
             if (merge_children && hx < 0) {  // H not precomputed (root level)
                 hx = free_buf((1u << ci) | (1u << li) | (1u << ri));
-                cta_merge_half<Key, K, T, false, false>(L, R, buf(hx), threadIdx.x, T);
+                grp_merge_half<Key, K, T / 32, false, false>(L, R, buf(hx), threadIdx.x >> 5);
                 // every thread reads H's ends below (merge_cur decides the
                 // buffer plan), so the whole CTA waits for it
                 __syncthreads();
@@ -1970,7 +1967,7 @@ struct HeapCta {
             if (!merge_cur)  // early stop ruled out the ordered case: a full inversion
                 cta_store<Key, T>(node(cur), hdata, K);
             else
-                cta_merge_half<Key, K, T, false, true>(cur_s, hdata, node(cur), threadIdx.x, T);
+                grp_merge_half<Key, K, T / 32, false, true>(cur_s, hdata, node(cur), threadIdx.x >> 5);
             const unsigned long long tl3 = now();
             __syncthreads();
             // The release fence waits for the batch's stores to be acked; a
@@ -1993,12 +1990,23 @@ struct HeapCta {
             bool h2 = false;
             if constexpr (kSplit) {
                 if (threadIdx.x < kHalf) {
-                    if (merge_cur) cta_merge_half<Key, K, T, true, false>(cur_s, hdata, buf(nxi), threadIdx.x, kHalf);
-                    if (merge_children) {
-                        cta_merge_half<Key, K, T, true, true>(L, R, node(lo), threadIdx.x, kHalf);
-                        grp_sync(1, kHalf);
-                        if (leader() && lo_locked) lane_unlock(lo, lo_rel);
+                    // the carried batch and the lo child's batch side by side
+                    // on two quarter groups (one after the other below 128
+                    // threads)
+                    constexpr int kQW = kHalf / 64;
+                    const uint32_t w = threadIdx.x >> 5;
+                    if constexpr (kQW >= 1) {
+                        if (w < (uint32_t)kQW) {
+                            if (merge_cur) grp_merge_half<Key, K, kQW, true, false>(cur_s, hdata, buf(nxi), w);
+                        } else if (merge_children) {
+                            grp_merge_half<Key, K, kQW, true, true>(L, R, node(lo), w - kQW);
+                        }
+                    } else {
+                        if (merge_cur) grp_merge_half<Key, K, 1, true, false>(cur_s, hdata, buf(nxi), 0);
+                        if (merge_children) grp_merge_half<Key, K, 1, true, true>(L, R, node(lo), 0);
                     }
+                    grp_sync(1, kHalf);
+                    if (merge_children && leader() && lo_locked) lane_unlock(lo, lo_rel);
                 } else {
                     acquire_children(hi, buf(li2), buf(ri2), kHalf, kHalf, 2);
                     // the next level's H, if its children interleave (the same
@@ -2007,7 +2015,7 @@ struct HeapCta {
                     const Key* R2 = buf(ri2);
                     const bool e2 = !sh->lk || L2[0] == kMaxKey || !sh->rk || R2[0] == kMaxKey;
                     if (!e2 && !(elide && !needs_merge_full<Key, K>(L2, R2)))
-                        cta_merge_half<Key, K, T, false, false>(L2, R2, buf(hx2), threadIdx.x - kHalf, kHalf);
+                        grp_merge_half<Key, K, kHalf / 32, false, false>(L2, R2, buf(hx2), (threadIdx.x - kHalf) >> 5);
                 }
                 __syncthreads();
                 const Key* L2 = buf(li2);
@@ -2018,8 +2026,8 @@ struct HeapCta {
                 li = li2;
                 ri = ri2;
             } else {
-                if (merge_cur) cta_merge_half<Key, K, T, true, false>(cur_s, hdata, buf(nxi), threadIdx.x, T);
-                if (merge_children) cta_merge_half<Key, K, T, true, true>(L, R, node(lo), threadIdx.x, T);
+                if (merge_cur) grp_merge_half<Key, K, T / 32, true, false>(cur_s, hdata, buf(nxi), threadIdx.x >> 5);
+                if (merge_children) grp_merge_half<Key, K, T / 32, true, true>(L, R, node(lo), threadIdx.x >> 5);
                 __syncthreads();
                 if (leader() && lo_locked && merge_children) lane_unlock(lo, lo_rel);
                 have = false;

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(T) merge_rows_kernel(const Key* a, const Key* 
         cta_load<Key, T>(sa, a + row * K, K);
         cta_load<Key, T>(sb, b + row * K, K);
         __syncthreads();
-        cta_merge_full<Key, K, T>(sa, sb, hi + row * K, lo + row * K);
+        cta_merge_full_bt<Key, K, T>(sa, sb, hi + row * K, lo + row * K);
         __syncthreads();
     }
 }
@@ -159,8 +159,12 @@ int launch_merge_k(const void* a, const void* b, void* hi, void* lo, uint64_t ro
     return note_cuda(cudaGetLastError());
 }
 
+#ifdef BH_DEV_KS  // development builds: a few node sizes only (fast compiles)
+#define BH_FOR_EACH_K(X) X(2) X(32) X(256) X(1024)
+#else
 #define BH_FOR_EACH_K(X) \
     X(1) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
+#endif
 
 template <typename Key>
 int dispatch_ops(const HeapView& hv, const RunView& rv, uint32_t ctas, cudaStream_t s) {

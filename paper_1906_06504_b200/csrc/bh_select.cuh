@@ -8,8 +8,10 @@
 //     latency) and merges it in registers with selects;
 //   * a level needs the two halves of a merge at different times, so the
 //     merge is split into half merges (outputs [0,K) or [K,2K)).
-// Variants measured and rejected (warp-tile bitonic, quaternary search,
-// vector windows, padded layouts, register sorts) live with their
+// The half merges of the heap use the warp-tile bitonic merge at the end of
+// this file (warp_half_bt); the per-thread merge path above remains for
+// unequal lengths and K < 32.  Variants measured and rejected (quaternary
+// search, vector windows, padded layouts, register sorts) live with their
 // microbenchmark in tools/microbench/mb_variants.cuh.
 #pragma once
 
@@ -138,6 +140,130 @@ __device__ __forceinline__ void cta_merge_half_p(const Key* __restrict__ A, cons
         merge_window<Key, P>(A, i, K, B, d0 - i, K, run);
         if constexpr (Global) store_run_cg<Key, P>(out + t0, run);
         else store_run<Key, P>(out + t0, run);
+    }
+}
+
+// ------------------------------------------------ warp-tile bitonic half --
+// One half of merge_and_sort(A, B) on two sorted K-batches, by the NW warps
+// of a thread group (`gw` = the calling warp's index within the group; all 32
+// lanes of each warp call).  Each warp owns a tile of 32E consecutive
+// outputs [D, D + 32E):
+//   1. the merge-path split of diagonal D (how many A keys precede output D)
+//      by a fixed-trip 32-ary search: lane l tests lo + (l+1)g for an odd
+//      stride g (32 probes never share a bank), ballot + popc, the range
+//      shrinks 32x per round (two rounds up to K = 1024);
+//   2. the tile is the 32E smallest keys of the windows A[a, a+32E) and
+//      B[b, b+32E) (sentinel past the ends), and min(Aw[i], Bw[32E-1-i]) is
+//      a bitonic sequence holding exactly them;
+//   3. a bitonic half-cleaner network sorts it: strides >= 32 inside each
+//      lane's registers, strides < 32 with warp shuffles.  Lane l ends with
+//      outputs D + 32e + l (coalesced stores).
+// Keys carry no payload, so the output equals the reference's stable
+// merge_sorted (proj/src/batch.cpp:21-42) key for key.  Measured (tools/
+// microbench `mb bt`, K=1024, 4 warps): 695 cycles per half vs 1954 for the
+// per-thread merge path on the same 128 threads (1089 on 256).
+// Not inlined: inlined into heap_ops_kernel (CUDA 12.9 ptxas, sm_100a) the
+// second-half tiles computed by warps 0-2 in heapify's phase 2 came out wrong
+// for correct, stable inputs -- deterministically, and again when recomputed
+// after a barrier -- while the same inputs replayed standalone
+// (tools/microbench/bt_check <dump>) and the out-of-line function are right.
+template <typename Key, int K, int E, bool Global>
+__device__ __noinline__ void warp_half_bt(const Key* __restrict__ A, const Key* __restrict__ B,
+                                             Key* __restrict__ out, uint32_t D) {
+    constexpr uint32_t W = 32u * E;
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t lo = D > (uint32_t)K ? D - K : 0u;
+    uint32_t hi = D < (uint32_t)K ? D : (uint32_t)K;
+#pragma unroll
+    for (uint32_t span = (uint32_t)K; span > 0; span >>= 5) {
+        const uint32_t g = span > 32 ? ((span + 31u) >> 5) | 1u : 1u;
+        const uint32_t p = lo + (lane + 1u) * g;
+        const bool ok = p <= hi && A[p - 1] <= B[D - p];
+        lo += (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, ok)) * g;
+        const uint32_t h2 = lo + g - 1u;
+        hi = h2 < hi ? h2 : hi;
+        if (g == 1u) break;
+    }
+    const uint32_t a = lo, b = D - lo;
+    Key v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const uint32_t i = e * 32u + lane;
+        const Key x = a + i < (uint32_t)K ? A[a + i] : KeyLimits<Key>::kMax;
+        const uint32_t j = b + (W - 1u - i);
+        const Key y = j < (uint32_t)K ? B[j] : KeyLimits<Key>::kMax;
+        v[e] = x < y ? x : y;
+    }
+#pragma unroll
+    for (int rs = E / 2; rs >= 1; rs >>= 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e & rs) == 0) {
+                const Key x = v[e], y = v[e + rs];
+                v[e] = x < y ? x : y;
+                v[e + rs] = x < y ? y : x;
+            }
+        }
+    }
+#pragma unroll
+    for (int ls = 16; ls >= 1; ls >>= 1) {
+        const bool upper = (lane & (uint32_t)ls) != 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const Key o = __shfl_xor_sync(0xFFFFFFFFu, v[e], ls);
+            v[e] = upper ? (v[e] < o ? o : v[e]) : (v[e] < o ? v[e] : o);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if constexpr (Global) __stcg(out + e * 32u + lane, v[e]);
+        else out[e * 32u + lane] = v[e];
+    }
+}
+
+// Tile shape of a half merge on NW warps: each used warp covers kPer outputs
+// in tiles of 32E (E <= 16 keys per lane).
+template <int K, int NW>
+struct TileShape {
+    static constexpr int kUsed = K >= 32 * NW ? NW : (K >= 32 ? K / 32 : 0);  // 0: K < 32
+    static constexpr int kPer = kUsed ? K / kUsed : 0;
+    static constexpr int E = kPer / 32 > 16 ? 16 : kPer / 32;
+    static constexpr int kTiles = E ? kPer / (32 * E) : 0;
+};
+
+// Outputs [0, K) (!Second) or [K, 2K) (Second) of merge(A, B) -> out[0, K),
+// by the NW warps of a group (gw = warp index in the group).  K < 32 falls
+// back to the per-thread merge path on the group's threads.  No barrier.
+template <typename Key, int K, int NW, bool Second, bool Global>
+__device__ __forceinline__ void grp_merge_half(const Key* __restrict__ A, const Key* __restrict__ B,
+                                               Key* __restrict__ out, uint32_t gw) {
+    using S = TileShape<K, NW>;
+    if constexpr (S::kUsed == 0) {
+        cta_merge_half<Key, K, 32 * NW, Second, Global>(A, B, out, gw * 32u + (threadIdx.x & 31u), 32u * NW);
+    } else {
+        if (gw >= (uint32_t)S::kUsed) return;
+#pragma unroll 1
+        for (int t = 0; t < S::kTiles; ++t) {
+            const uint32_t o = gw * (uint32_t)S::kPer + (uint32_t)t * 32u * S::E;
+            warp_half_bt<Key, K, S::E, Global>(A, B, out + o, (Second ? (uint32_t)K : 0u) + o);
+        }
+    }
+}
+
+// merge_and_sort of two full K-batches on T threads: the first half on warps
+// [0, T/64), the second on the rest (side by side).  No barrier.
+template <typename Key, int K, int T, bool HiGlobal = false, bool LoGlobal = false>
+__device__ __forceinline__ void cta_merge_full_bt(const Key* __restrict__ A, const Key* __restrict__ B,
+                                                  Key* __restrict__ out_hi, Key* __restrict__ out_lo) {
+    constexpr int kW = T / 32;
+    if constexpr (kW >= 2) {
+        constexpr int kH = kW / 2;
+        const uint32_t w = threadIdx.x >> 5;
+        if (w < (uint32_t)kH) grp_merge_half<Key, K, kH, false, HiGlobal>(A, B, out_hi, w);
+        else if (w < 2u * kH) grp_merge_half<Key, K, kH, true, LoGlobal>(A, B, out_lo, w - kH);
+    } else {
+        grp_merge_half<Key, K, 1, false, HiGlobal>(A, B, out_hi, 0);
+        grp_merge_half<Key, K, 1, true, LoGlobal>(A, B, out_lo, 0);
     }
 }
 

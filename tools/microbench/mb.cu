@@ -180,6 +180,119 @@ void run_half(const char* name) {
     cudaFree(d); cudaFree(sink); cudaFree(o);
 }
 
+// Warp-tile bitonic half merge (candidate for the product): each warp owns a
+// tile of 32E consecutive outputs [D, D + 32E) of merge(A, B).  (1) The
+// merge-path split of diagonal D by a fixed-trip 32-ary search (lane l tests
+// lo + (l+1)g with an odd stride g, ballot + popc; two rounds for K <= 1024).
+// (2) The tile = the 32E smallest of the windows A[a, a+32E) and B[b, b+32E)
+// (sentinel past the ends): min(Aw[i], Bw[32E-1-i]) is bitonic and holds
+// exactly them.  (3) A bitonic half-cleaner network sorts it: strides >= 32
+// in registers, below with shuffles.  Lane l ends with outputs D + 32e + l.
+template <typename Key, int K, int E>
+__device__ __forceinline__ void warp_half_bt(const Key* __restrict__ A, const Key* __restrict__ B,
+                                             Key* __restrict__ out, uint32_t D) {
+    constexpr uint32_t W = 32u * E;
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t lo = D > (uint32_t)K ? D - K : 0u;
+    uint32_t hi = D < (uint32_t)K ? D : (uint32_t)K;
+    // fixed trips: each round shrinks the range by 32
+#pragma unroll
+    for (uint32_t span = (uint32_t)K; span > 0; span >>= 5) {
+        const uint32_t g = span > 32 ? ((span + 31u) >> 5) | 1u : 1u;
+        const uint32_t p = lo + (lane + 1u) * g;
+        const bool ok = p <= hi && A[p - 1] <= B[D - p];
+        const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, ok));
+        lo += c * g;
+        const uint32_t h2 = lo + g - 1u;
+        hi = h2 < hi ? h2 : hi;
+        if (g == 1u) break;
+    }
+    const uint32_t a = lo, b = D - lo;
+    Key v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const uint32_t i = e * 32u + lane;
+        const Key x = a + i < (uint32_t)K ? A[a + i] : KeyLimits<Key>::kMax;
+        const uint32_t j = b + (W - 1u - i);
+        const Key y = j < (uint32_t)K ? B[j] : KeyLimits<Key>::kMax;
+        v[e] = x < y ? x : y;
+    }
+#pragma unroll
+    for (int rs = E / 2; rs >= 1; rs >>= 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e & rs) == 0) {
+                const Key x = v[e], y = v[e + rs];
+                v[e] = x < y ? x : y;
+                v[e + rs] = x < y ? y : x;
+            }
+        }
+    }
+#pragma unroll
+    for (int ls = 16; ls >= 1; ls >>= 1) {
+        const bool upper = (lane & ls) != 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const Key o = __shfl_xor_sync(0xFFFFFFFFu, v[e], ls);
+            v[e] = upper ? (v[e] < o ? o : v[e]) : (v[e] < o ? v[e] : o);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) out[D + e * 32u + lane] = v[e];
+}
+
+template <typename Key, int K, int T, int E>
+__global__ void __launch_bounds__(T) halfbt_bench(const Key* in, int iters, unsigned long long* out, Key* sink) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    Key* A = reinterpret_cast<Key*>(sm);
+    Key* B = A + K;
+    Key* H = B + K;
+    for (int i = threadIdx.x; i < 2 * K; i += T) A[i] = in[i];
+    __syncthreads();
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        for (uint32_t D = (threadIdx.x >> 5) * 32u * E; D < (uint32_t)K; D += (T / 32) * 32u * E)
+            warp_half_bt<Key, K, E>(A, B, H, D);
+        __syncthreads();
+        if (threadIdx.x == 0) A[0] = H[0] < A[0] ? H[0] : A[0];
+        __syncthreads();
+    }
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) out[0] = (t1 - t0) / iters;
+    for (int i = threadIdx.x; i < K; i += T) sink[i] = H[i];
+}
+
+template <int K, int T, int E>
+void run_halfbt(const char* name) {
+    using Key = uint32_t;
+    std::mt19937 rng(1);
+    std::vector<Key> h(2 * K);
+    for (auto& x : h) x = rng() >> 1;
+    std::sort(h.begin(), h.begin() + K);
+    std::sort(h.begin() + K, h.end());
+    Key *d, *sink;
+    unsigned long long* o;
+    CK(cudaMalloc(&d, 2 * K * 4));
+    CK(cudaMalloc(&sink, 2 * K * 4 + 16));
+    CK(cudaMalloc(&o, 8 * 8));
+    CK(cudaMemcpy(d, h.data(), 2 * K * 4, cudaMemcpyHostToDevice));
+    auto kern = halfbt_bench<Key, K, T, E>;
+    const int smem = 3 * K * 4 + 64;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<1, T, smem>>>(d, 1, o, sink);
+    CK(cudaDeviceSynchronize());
+    std::vector<Key> got(K), ref(2 * K);
+    CK(cudaMemcpy(got.data(), sink, K * 4, cudaMemcpyDeviceToHost));
+    std::merge(h.begin(), h.begin() + K, h.begin() + K, h.end(), ref.begin());
+    if (!std::equal(got.begin(), got.end(), ref.begin())) printf("halfbt %s WRONG OUTPUT\n", name);
+    kern<<<1, T, smem>>>(d, 2000, o, sink);
+    CK(cudaDeviceSynchronize());
+    unsigned long long c;
+    CK(cudaMemcpy(&c, o, 8, cudaMemcpyDeviceToHost));
+    printf("halfbt %-21s K=%d T=%d E=%d : %llu cycles\n", name, K, T, E, c);
+    cudaFree(d); cudaFree(sink); cudaFree(o);
+}
+
 template <typename Key, int K, int T, int V>
 __global__ void __launch_bounds__(T) merge_bench(const Key* in, int iters, unsigned long long* out, Key* sink) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -534,6 +647,33 @@ int main(int argc, char** argv) {
             run_half<1024, 512, 8, 1>("quaternary");
             run_half<1024, 512, 1, 1>("quaternary");
             run_half<1024, 256, 4, 1>("quaternary");
+        }
+        if (w == "bt") {
+            run_halfbt<1024, 128, 8>("warp bitonic");
+            run_halfbt<1024, 256, 4>("warp bitonic");
+            run_halfbt<1024, 512, 2>("warp bitonic");
+            run_halfbt<1024, 256, 2>("warp bitonic 2 tiles");
+            run_halfbt<1024, 512, 1>("warp bitonic 2 tiles");
+            run_halfbt<2048, 512, 4>("warp bitonic");
+            run_halfbt<2048, 256, 8>("warp bitonic");
+            run_halfbt<256, 64, 4>("warp bitonic");
+            run_halfbt<256, 128, 2>("warp bitonic");
+            run_half<1024, 256, 4, 0>("binary");
+            run_half<1024, 512, 2, 0>("binary");
+        }
+        if (w == "groups") {  // half merge on one thread group of T threads (P outputs each)
+            run_half<1024, 128, 8, 0>("binary");
+            run_half<1024, 256, 4, 0>("binary");
+            run_half<1024, 512, 2, 0>("binary");
+            run_half<1024, 1024, 1, 0>("binary");
+            run_half<1024, 128, 8, 1>("quaternary");
+            run_half<1024, 256, 4, 1>("quaternary");
+            run_half<256, 64, 4, 0>("binary");
+            run_half<256, 32, 8, 0>("binary");
+            run_half<2048, 256, 8, 0>("binary");
+            run_half<2048, 512, 4, 0>("binary");
+            run_lat<128, 2>("bar");
+            run_lat<256, 2>("bar");
         }
         if (w == "load") {
             run_nodeload<16, 256>("remote-written");
