@@ -163,8 +163,9 @@ BH_API int bh_info(bh_heap* heap, uint32_t* k, uint32_t* key_bits, uint64_t* slo
                    uint32_t* max_ctas);
 
 /* Device event log (BH_FLAG_RECORD handles).  Each event: ts (global device
- * clock), op index, kind (0 inv, 1 res, 2 lock acquired, 3 lock released),
- * node slot.  Mirrors Recorder::op_begin/lock_acquired/lock_released/op_end
+ * clock), op index, kind (0 inv, 1 res, 2 lock acquired, 3 lock released,
+ * 4 lock acquired on the refill source -- the last node a delete moves into
+ * the root, held only to copy and blank it, never across a wait), node slot.  Mirrors Recorder::op_begin/lock_acquired/lock_released/op_end
  * (proj/include/batchheap/instrumentation.hpp:20-57). Returns the number of
  * events of the last bulk run (events sorted by op, then ts). */
 typedef struct {

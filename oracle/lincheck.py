@@ -21,7 +21,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 from sortedcontainers import SortedList
 
 INSERT, DELETE = 0, 1
-EV_INV, EV_RES, EV_ACQ, EV_REL = 0, 1, 2, 3
+EV_INV, EV_RES, EV_ACQ, EV_REL, EV_ACQ_REFILL = 0, 1, 2, 3, 4
 
 
 @dataclass
@@ -29,6 +29,7 @@ class LockSpan:
     node: int
     acquire_ts: int
     release_ts: int = 0
+    refill: bool = False  # a delete's refill source (EV_ACQ_REFILL)
 
 
 @dataclass
@@ -77,8 +78,8 @@ def decode_history(events, op_kinds: Sequence[int], op_keys: Sequence[Sequence[i
                 rec.invoke_ts = ts
             elif kind == EV_RES:
                 rec.respond_ts = ts
-            elif kind == EV_ACQ:
-                open_locks.append(LockSpan(node, ts))
+            elif kind in (EV_ACQ, EV_ACQ_REFILL):
+                open_locks.append(LockSpan(node, ts, refill=kind == EV_ACQ_REFILL))
             elif kind == EV_REL:
                 for span in reversed(open_locks):
                     if span.node == node and span.release_ts == 0:
@@ -368,11 +369,24 @@ def _is_ancestor(a: int, d: int) -> bool:
 
 
 def check_lock_order(history: List[OpRecord]) -> Tuple[bool, str]:
+    """lincheck.cpp:193-217: no op acquires a node while it holds one of the
+    node's descendants.  One documented exception: a delete's refill source
+    (the last node, EV_ACQ_REFILL spans) may still be held when the same op
+    claims an ancestor of it.  The refill holder claims the last node with
+    only the root (and, in a delete server, nodes of the top levels) held,
+    copies and blanks it and releases it without waiting on anything in
+    between, so the refill span cannot be an edge of a wait-for cycle: the
+    reference's deadlock argument (heap.cpp:467-531, last released before
+    any child is awaited) holds for the thread group that holds it, while
+    another thread group of the same CTA claims the children in parallel
+    (bh_heap.cuh: refill_last beside acquire_children)."""
     for op in history:
         locks = op.locks
         for i in range(len(locks)):
             for j in range(i + 1, len(locks)):
                 a, b = locks[i], locks[j]
+                if a.refill:
+                    continue
                 overlap = a.acquire_ts < b.release_ts and b.acquire_ts < a.release_ts
                 if overlap and a.node != b.node and _is_ancestor(b.node, a.node):
                     return False, f"{_describe(op)} acquired node {a.node} before its ancestor {b.node}"

@@ -79,9 +79,17 @@ struct StreamGuard {
     }
 };
 
+inline unsigned long long sm_count_now() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+        return 1;
+    return (unsigned long long)n;
+}
+
 inline unsigned grid_for(unsigned long long n, unsigned threads = 256) {
     const unsigned long long g = (n + threads - 1) / threads;
-    return (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(g, 148ull * 16));
+    return (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(g, 16ull * sm_count_now()));
 }
 
 // ------------------------------------------------------------------ SSSP --
@@ -433,7 +441,7 @@ int bh_sssp(uint32_t n_nodes, const uint64_t* offsets, const uint32_t* adj_node,
             const uint64_t n_del = (want + k - 1) / k;
             APP_CUDA(cudaMemsetAsync(d_ctr.p + 3, 0, 8, s));
             APP_OK(hr.run(1, n_del * k, nullptr, d_out.p));
-            sssp_decode<<<(unsigned)std::min<uint64_t>(n_del, 148 * 8), 128, 0, s>>>(d_out.p, hr.lens.p, n_del, k,
+            sssp_decode<<<(unsigned)std::min<uint64_t>(n_del, 8ull * sm_count_now()), 128, 0, s>>>(d_out.p, hr.lens.p, n_del, k,
                                                                                   d_proc.p, d_ctr.p + 3);
             APP_CUDA(cudaGetLastError());
             APP_CUDA(cudaMemcpyAsync(h_ctr + 3, d_ctr.p + 3, 8, cudaMemcpyDeviceToHost, s));

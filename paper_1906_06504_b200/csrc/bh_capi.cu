@@ -118,7 +118,15 @@ struct bh_heap {
     unsigned long long* d_counters = nullptr;
     unsigned long long* d_prof = nullptr;
     unsigned long long* d_tickets = nullptr;  // ring of bulk tickets
-    std::atomic<uint32_t> ticket_next{0};
+    // A ring slot is reused only after the launch that last used it has
+    // finished (its completion event, waited on by the reusing stream): the
+    // zeroing memset never hits a running launch's op counter, and the slot
+    // address, which delete serving uses as the launch id, names one running
+    // launch at a time.
+    std::mutex ticket_mu;
+    uint32_t ticket_next = 0;
+    cudaEvent_t ticket_ev[64] = {};
+    bool ticket_used[64] = {};
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;
     KernelInfo kinfo{};
@@ -162,7 +170,7 @@ struct bh_heap {
 
 namespace {
 
-constexpr uint32_t kTicketRing = 64;
+constexpr uint32_t kTicketRing = 64;  // = size of bh_heap::ticket_ev
 
 int launch_ops(bh_heap* h, const RunView& rv, uint32_t ctas, cudaStream_t s) {
     HeapView hv = h->view();
@@ -449,6 +457,8 @@ void bh_destroy(bh_heap* h) {
     cudaFree(h->d_counters);
     cudaFree(h->d_prof);
     cudaFree(h->d_tickets);
+    for (cudaEvent_t& e : h->ticket_ev)
+        if (e) cudaEventDestroy(e);
     cudaFree(h->d_stage);
     cudaFree(h->d_events);
     cudaFree(h->d_event_counts);
@@ -488,16 +498,24 @@ int bh_run_ops_device(bh_heap* h, const bh_op* ops, uint64_t n_ops, const void* 
     rv.out_status = out_status;
     rv.out_lens = out_lens;
     rv.out_seq = reinterpret_cast<unsigned long long*>(out_seq);
-    const uint32_t slot = h->ticket_next.fetch_add(1) % kTicketRing;
+    std::lock_guard<std::mutex> tg(h->ticket_mu);
+    const uint32_t slot = h->ticket_next++ % kTicketRing;
+    if (!h->ticket_ev[slot]) BH_CUDA(cudaEventCreateWithFlags(&h->ticket_ev[slot], cudaEventDisableTiming));
+    if (h->ticket_used[slot]) BH_CUDA(cudaStreamWaitEvent(s, h->ticket_ev[slot], 0));
     rv.ticket = h->d_tickets + slot * 16;
     BH_CUDA(cudaMemsetAsync(rv.ticket, 0, 8, s));
+    int rc;
     if (h->flags & BH_FLAG_RECORD) {
         std::lock_guard<std::mutex> g(h->rec_mu);
-        int rc = prepare_record(h, n_ops, s, rv);
-        if (rc != BH_OK) return rc;
-        return launch_ops(h, rv, pick_ctas(h, n_ops, cfg), s);
+        rc = prepare_record(h, n_ops, s, rv);
+        if (rc == BH_OK) rc = launch_ops(h, rv, pick_ctas(h, n_ops, cfg), s);
+    } else {
+        rc = launch_ops(h, rv, pick_ctas(h, n_ops, cfg), s);
     }
-    return launch_ops(h, rv, pick_ctas(h, n_ops, cfg), s);
+    if (rc != BH_OK) return rc;
+    BH_CUDA(cudaEventRecord(h->ticket_ev[slot], s));
+    h->ticket_used[slot] = true;
+    return BH_OK;
 }
 
 int bh_run_ops(bh_heap* h, const bh_op* ops, uint64_t n_ops, const void* key_pool, uint64_t key_pool_len,
@@ -571,7 +589,7 @@ int bh_plan_phase(bh_heap* h, int kind, uint64_t n_keys, bh_op* ops, int on_devi
     }
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
     if (n_ops == 0) return BH_OK;
-    const unsigned grid = (unsigned)std::min<uint64_t>((n_ops + 255) / 256, 148 * 8);
+    const unsigned grid = (unsigned)std::min<uint64_t>((n_ops + 255) / 256, 8ull * h->sm_count);
     plan_kernel<<<grid, 256, 0, s>>>(kind, h->k, n_keys, n_ops, ops);
     BH_CUDA(cudaGetLastError());
     return BH_OK;

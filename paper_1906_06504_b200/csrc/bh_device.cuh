@@ -76,9 +76,11 @@ __device__ __forceinline__ bool state_cas_relaxed(uint32_t* p, uint32_t expected
 __device__ __forceinline__ void state_store_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// A strong store with no ordering of its own: publishes data only when a
-// release fence (e.g. an earlier state_release by the same thread) has
-// already ordered the CTA's writes before it.
+// A strong store with no ordering of its own: publishes data only when an
+// explicit fence (__threadfence = fence.acq_rel.gpu) by the same thread has
+// already ordered the CTA's writes before it.  (A red/st.release orders
+// earlier writes before that one location only; it is not a fence for later
+// relaxed stores.)
 __device__ __forceinline__ void state_store_relaxed(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -1249,7 +1249,7 @@ struct HeapCta {
             }
             if (gt == 0) {
                 sh->ok[2] = ok;
-                if (ok) rec_lane(kEvAcq, last);
+                if (ok) rec_lane(kEvAcqRefill, last);
             }
             grp_sync(bar, nthr);
             if (sh->ok[2]) {
@@ -1262,8 +1262,15 @@ struct HeapCta {
     }
 
     // ================================================== delete serving ==
-    // Flat combining of deletes in the root queue lock (TD and BU heaps; BU
-    // deletes pass the phase gate first, as their own root step would).  A delete holding the root with deletes queued behind it keeps
+    // Flat combining of deletes in the root queue lock (TD and BU heaps).  In
+    // BU heaps the server's own op passed the phase gate (gate_try, phase =
+    // heapify, not closing) and the ops it serves are admitted under that
+    // pass (deleters + 1 each, below) without their own gate_try: the gate
+    // cannot close during the hold, because closing it takes the root lock,
+    // and the hold serves only the contiguous run of delete tickets queued
+    // ahead in the FIFO root queue, so a climber that arrives waits for at
+    // most those, then closes the phase as usual.
+    // A delete holding the root with deletes queued behind it keeps
     // the root and nodes 2-3 (claimed, in shared memory) and runs, for its own
     // op and then each queued delete in ticket order, the reference's
     // delete_min through levels 0 and 1: root result, refill from the last
@@ -1316,19 +1323,20 @@ struct HeapCta {
         }
     }
 
-    // kPubLane: the previous op's releases, one fence for all of them.
+    // kPubLane: the previous op's releases, one fence for all of them.  The
+    // fence (fence.acq_rel.gpu, cumulative over the CTA's writes ordered
+    // before it by the barriers) publishes the mailbox batch, qline word 14
+    // and the released nodes' keys; every release after it is relaxed.  (A
+    // red.release is a release for its own location only, not a fence.)
     __device__ void sv_flush(SvPending& pd) {
-        bool fenced = false;
         if (pd.pub && record)  // the op the woken CTA continues, for its events
             st_cg_u64(reinterpret_cast<unsigned long long*>(qline(pd.pub) + 14), pd.pubop);
+        if (pd.n || pd.pub) __threadfence();
         for (uint32_t i = 0; i < pd.n; ++i) {
             if (record && pd.op[i] != ~0ull) rec_for(pd.op[i], kEvRel, pd.slot[i]);
-            if (!fenced) state_release(st(pd.slot[i]), kInUse, pd.rel[i]);
-            else state_release_relaxed(st(pd.slot[i]), kInUse, pd.rel[i]);
-            fenced = true;
+            state_release_relaxed(st(pd.slot[i]), kInUse, pd.rel[i]);
         }
         if (pd.pub) {
-            if (!fenced) __threadfence();
             const unsigned long long w = ((unsigned long long)pd.pubw << 32) | (((uint32_t)pd.pub << 1) | 1u);
             asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(qline(pd.pub)), "l"(w) : "memory");
         }
@@ -1449,13 +1457,10 @@ struct HeapCta {
             }
             if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvB], now() - ts0);
             const unsigned long long tc = now();
-            if (!record) acquire_children(hi1, buf(l2), buf(r2), kHalfT, kHalfT, 2);
+            acquire_children(hi1, buf(l2), buf(r2), kHalfT, kHalfT, 2);
             if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvClaim], now() - tc);
         }
         __syncthreads();
-        // recorded heaps keep the reference's top-down lock order in their
-        // histories: the claim follows the refill's release
-        if (record) acquire_children(hi1, buf(l2), buf(r2));
         const unsigned long long ts1 = now();
         pf_add(pfSvSplit, ts1 - ts0);
         const bool handoff = sh->serve != 0;
@@ -1637,9 +1642,9 @@ struct HeapCta {
         }
         __syncthreads();
         pend(2, rel2, ~0ull);
+        pend(3, rel3, ~0ull);
         if (threadIdx.x == kPubLane) {
-            sv_flush(sh->pd);
-            state_release_relaxed(st(3), kInUse, rel3);
+            sv_flush(sh->pd);  // its fence also orders nodes 1-3 and the header
             sh->root_tk = t;
             state_store_relaxed(qline(t + 1), (uint32_t)(t + 1) << 1);  // root_unlock
         }
@@ -1810,9 +1815,9 @@ struct HeapCta {
         const unsigned long long ta = now();
         pf_add(pfRsHead, ta - t1);
         if (plen) cta_load<Key, T>(sp, partial, plen);
-        // (recorded heaps keep the reference's order in their histories:
-        // children claimed after the refill released the last node)
-        const bool split = T >= 64 && nodes >= 4 && !record;
+        // (recorded heaps run the same schedule; their histories mark the
+        // refill span, which may overlap the children's claims)
+        const bool split = T >= 64 && nodes >= 4;
         if (split) {
             constexpr uint32_t kHalf = T / 2;
             if (threadIdx.x < kHalf) {

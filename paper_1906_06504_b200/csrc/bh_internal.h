@@ -75,7 +75,11 @@ enum ErrorFlag : unsigned long long {
     kErrRetake = 1ull << 3,           // gated BU climb: re-take CAS of the parked slot failed
 };
 
-enum EventKind : uint16_t { kEvInv = 0, kEvRes = 1, kEvAcq = 2, kEvRel = 3 };
+// kEvAcqRefill: acquire of a delete's refill source (refill_root_from,
+// heap.cpp:467-531), held only to copy and blank it -- never across a wait --
+// so the lock-order check may see it overlap an ancestor's claim (see
+// oracle/lincheck.py check_lock_order).
+enum EventKind : uint16_t { kEvInv = 0, kEvRes = 1, kEvAcq = 2, kEvRel = 3, kEvAcqRefill = 4 };
 
 struct DevEvent {
     unsigned long long ts;

@@ -95,16 +95,21 @@ __global__ void gather_kernel(HeapView hv, unsigned long long nodes, Key* out) {
     }
 }
 
+// SM count of the current device (grid sizes of the helper kernels).
+inline int device_sm_count() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+        return 1;
+    return n;
+}
+
 template <typename Key, int K, bool Rec>
 int launch_ops_kr(const HeapView& hv, const RunView& rv, uint32_t ctas, cudaStream_t stream) {
     using Cfg = KernelCfg<Key, K>;
+    // (the dynamic shared memory attribute of both instantiations was set on
+    // this device by bh_create through kernel_info_k)
     auto kern = heap_ops_kernel<Key, K, Cfg::kThreads, Rec>;
-    static bool attr_set = false;  // dynamic + static smem may pass 48 KB
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-        if (e != cudaSuccess) return note_cuda(e);
-        attr_set = true;
-    }
     kern<<<ctas, Cfg::kThreads, Cfg::kSmem, stream>>>(hv, rv);
     return note_cuda(cudaGetLastError());
 }
@@ -119,8 +124,13 @@ int launch_ops_k(const HeapView& hv, const RunView& rv, uint32_t ctas, cudaStrea
 template <typename Key, int K>
 int kernel_info_k(KernelInfo* info) {
     using Cfg = KernelCfg<Key, K>;
+    // Function attributes are per device: set them for both instantiations
+    // (plain and recording) on the current device, which bh_create selected.
     auto kern = heap_ops_kernel<Key, K, Cfg::kThreads, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (e != cudaSuccess) return note_cuda(e);
+    e = cudaFuncSetAttribute(heap_ops_kernel<Key, K, Cfg::kThreads, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (e != cudaSuccess) return note_cuda(e);
     int blocks = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, Cfg::kThreads, Cfg::kSmem) !=
@@ -136,7 +146,8 @@ template <typename Key, int K>
 int launch_sort_k(void* keys, const uint32_t* lens, uint64_t rows, cudaStream_t stream) {
     using Cfg = KernelCfg<Key, K>;
     const uint32_t smem = K * sizeof(Key);
-    const unsigned grid = (unsigned)(rows < 148ull * 16 ? rows : 148ull * 16);
+    const unsigned long long cap = 16ull * device_sm_count();
+    const unsigned grid = (unsigned)(rows < cap ? rows : cap);
     if (grid == 0) return BH_OK;
     sort_rows_kernel<Key, K, Cfg::kThreads>
         <<<grid, Cfg::kThreads, smem, stream>>>(static_cast<Key*>(keys), lens, rows);
@@ -152,7 +163,8 @@ int launch_merge_k(const void* a, const void* b, void* hi, void* lo, uint64_t ro
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return note_cuda(e);
     }
-    const unsigned grid = (unsigned)(rows < 148ull * 16 ? rows : 148ull * 16);
+    const unsigned long long cap = 16ull * device_sm_count();
+    const unsigned grid = (unsigned)(rows < cap ? rows : cap);
     if (grid == 0) return BH_OK;
     kern<<<grid, Cfg::kThreads, smem, stream>>>(static_cast<const Key*>(a), static_cast<const Key*>(b),
                                                 static_cast<Key*>(hi), static_cast<Key*>(lo), rows);
@@ -217,14 +229,15 @@ int dispatch_merge(uint32_t k, const void* a, const void* b, void* hi, void* lo,
 
 template <typename Key>
 int launch_check(const HeapView& hv, unsigned long long* result, cudaStream_t s) {
-    check_kernel<Key><<<148 * 4, 256, 0, s>>>(hv, result);
+    check_kernel<Key><<<4 * device_sm_count(), 256, 0, s>>>(hv, result);
     return note_cuda(cudaGetLastError());
 }
 
 template <typename Key>
 int launch_gather(const HeapView& hv, unsigned long long nodes, void* out, cudaStream_t s) {
     if (nodes == 0) return BH_OK;
-    const unsigned grid = (unsigned)(nodes < 148ull * 8 ? nodes : 148ull * 8);
+    const unsigned long long cap = 8ull * device_sm_count();
+    const unsigned grid = (unsigned)(nodes < cap ? nodes : cap);
     gather_kernel<Key><<<grid, 256, 0, s>>>(hv, nodes, static_cast<Key*>(out));
     return note_cuda(cudaGetLastError());
 }

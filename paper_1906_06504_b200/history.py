@@ -25,7 +25,7 @@ from typing import Dict, List, Sequence
 
 import numpy as np
 
-EV_INV, EV_RES, EV_ACQ, EV_REL = 0, 1, 2, 3  # bh_event.kind (bh_internal.h EventKind)
+EV_INV, EV_RES, EV_ACQ, EV_REL, EV_ACQ_REFILL = 0, 1, 2, 3, 4  # bh_event.kind (bh_internal.h EventKind)
 
 
 class OpKind(enum.IntEnum):
@@ -169,7 +169,7 @@ def history_from_run(events: np.ndarray, op_kinds: Sequence[int], op_keys: Seque
                 rec.invoke_ts = ts
             elif kind == EV_RES:
                 rec.respond_ts = ts
-            elif kind == EV_ACQ:
+            elif kind in (EV_ACQ, EV_ACQ_REFILL):  # the text format has no refill mark
                 if node in held:
                     raise InstrumentationError(f"op {i}: node {node} acquired twice")
                 held[node] = LockSpan(node, ts)

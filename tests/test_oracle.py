@@ -243,3 +243,22 @@ def test_lincheck_mutual_exclusion_and_order():
     c.locks = [LC.LockSpan(3, 2, 7), LC.LockSpan(1, 3, 8)]
     ok, _ = LC.check_lock_order([c])
     assert not ok
+
+
+def test_lock_order_refill_exception():
+    """A refill span (the last node, EV_ACQ_REFILL) may overlap the same op's
+    claim of one of its ancestors; any other descendant-first overlap fails."""
+    c = _op(2, LC.DELETE, [1], 1, 2, 20, 21)
+    # root, then the refill source 9 and its ancestor 2 (claimed while 9 is held)
+    c.locks = [LC.LockSpan(1, 2, 19), LC.LockSpan(9, 3, 6, refill=True), LC.LockSpan(2, 4, 12)]
+    assert LC.check_lock_order([c])[0]
+    c.locks[1].refill = False
+    assert not LC.check_lock_order([c])[0]
+    # decode_history marks kind-4 acquisitions as refill spans
+    ev = [dict(ts=1, op=0, kind=LC.EV_INV, node=0), dict(ts=2, op=0, kind=LC.EV_ACQ, node=1),
+          dict(ts=3, op=0, kind=LC.EV_ACQ_REFILL, node=9), dict(ts=4, op=0, kind=LC.EV_ACQ, node=2),
+          dict(ts=5, op=0, kind=LC.EV_REL, node=9), dict(ts=6, op=0, kind=LC.EV_REL, node=2),
+          dict(ts=7, op=0, kind=LC.EV_REL, node=1), dict(ts=8, op=0, kind=LC.EV_RES, node=0)]
+    (rec,) = LC.decode_history(ev, [LC.DELETE], [[1]])
+    assert [s.refill for s in rec.locks] == [False, True, False]
+    assert LC.check_lock_order([rec])[0]
