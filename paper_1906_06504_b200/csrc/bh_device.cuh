@@ -130,6 +130,43 @@ __device__ __forceinline__ void grp_sync(uint32_t id, uint32_t nthr) {
         asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory");
 }
 
+// ------------------------------------------------------------ mbarriers --
+// Shared-memory mbarriers (sm_90+) for producer -> consumer hand-offs between
+// the warp roles of a delete server (bh_heap.cuh, serve3): the producer's
+// smem writes are released by its arrive, the consumer's wait acquires them.
+// Phase n of a barrier completes after `count` arrivals; a consumer of the
+// n-th completion waits for parity n & 1.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mb_init(unsigned long long* mb, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long* mb) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mb)) : "memory");
+}
+__device__ __forceinline__ bool mb_test(unsigned long long* mb, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(mb)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* mb, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(mb)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
 // Group versions of the node moves (thread `tid` of `nthr`).
 template <typename Key>
 __device__ __forceinline__ void grp_load(Key* __restrict__ s, const Key* __restrict__ g, uint32_t n, uint32_t tid,

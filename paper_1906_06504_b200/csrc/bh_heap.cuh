@@ -59,6 +59,49 @@ struct SvPending {
     unsigned long long pubop;  // op whose continuation it is (recorded heaps)
 };
 
+// A served op's record for the control warp of a three-level delete server
+// (ring of 4, by the op's index in the hold).
+struct Sv3Rec {
+    unsigned long long op, off, seq, t, cont;
+    unsigned long long relslot[2];
+    uint32_t relst[2];
+    uint32_t nrel, crel;
+    uint32_t rootbuf;  // the op's result: node 1 before the op
+    uint32_t c3buf;    // carried batch still to copy into mbox(t + 1) (~0: already there)
+    uint32_t cnt_merges, cnt_elided, cnt_early, cnt_visits;
+    uint32_t last;     // the hold ends after this op
+};
+
+// Shared state of a three-level delete server (serve3): mbarriers between
+// its warp roles, the messages they pass, the look-ahead ring.
+struct Sv3Shared {
+    unsigned long long mb_go[2];   // merge leader -> refill warp g: a refill to run (g = op parity)
+    unsigned long long mb_rf[2];   // refill warp g -> merge warps: refill batch in smem
+    unsigned long long mb_c3;      // claim warp -> merge warps: level-3 children in smem
+    unsigned long long mb_go3;     // merge leader -> claim warp: the op's level-3 claim
+    unsigned long long mb_rec;     // merge leader -> control warp: the op's record
+    unsigned long long g3_t, g3_op;
+    uint32_t g3_hi2, g3_L, g3_R;   // hi2 (0 = leave the loop), destination buffers
+    uint32_t g3_j;
+    unsigned long long go_last[2]; // refill source rank (0 = leave the loop)
+    unsigned long long go_op[2];   // op index (event log)
+    uint32_t go_buf[2];            // destination buffer
+    uint32_t go_j[2];              // the op's index in the hold (timeline)
+    uint32_t lk3, lrel3, rk3, rrel3;  // level-3 claim results
+    uint32_t hold_on[2];           // merge leader -> merge warps: serve op j+1 (by op parity)
+    unsigned long long nx_op[2], nx_off[2];
+    volatile uint32_t w0_done;     // ops the control warp has finished
+    volatile uint32_t w0_seen;     // op records the control warp has taken (mb_rec phases seen)
+    uint32_t nb_end[8];            // node map at the hold's end
+    Sv3Rec rec[4];
+    // claim warp's look-ahead ring: confirmed waiting deletes by ticket % 8
+    unsigned long long la_tk[8], la_op[8], la_off[8];
+    // level-3 state words (slots 8-15) a claim may CAS from directly: the
+    // words the server's own releases produce, and the claimed words
+    uint32_t w3pred[8];
+    uint32_t w3in[8];
+};
+
 struct OpShared {
     unsigned long long op;
     unsigned long long nodes;
@@ -80,6 +123,18 @@ struct OpShared {
     uint32_t contw;                // served delete: continuation slot | kDelMod bit 31
     uint32_t next_w;               // delete server: pre-observed state word of the next refill
     SvPending pd;
+    Sv3Shared s3;
+    unsigned long long tl[16 * 24];  // profiling: per-op clocks of a three-level server (kTlSmemOps ops)
+};
+constexpr uint32_t kTlSmemOps = 16;
+
+// Three-level delete server: node sizes whose 24 buffers fit in shared memory
+// next to everything else, on 512-thread CTAs (16 warps: control, claim,
+// 12 merge warps, 2 refill warps).
+template <typename Key, int K, int T>
+struct Serve3Cfg {
+    static constexpr int kBufs = 24;
+    static constexpr bool kOn = T == 512 && (unsigned long long)kBufs * K * sizeof(Key) <= 200ull * 1024ull;
 };
 
 // Profile slots (BH_FLAG_PROFILE): SM cycles summed over ops by the leader.
@@ -122,6 +177,22 @@ enum ProfIdx {
     pfSvR3,     //   level-1 merges, lo2 write and release
     pfSvNext,   //   next-waiter check and continuation hand-off
     pfSvClaim,  //   level-2 claim (after H0 || lo0)
+    // three-level delete server (serve3), per op, cycles
+    pf3Ops,     // ops run by a three-level server
+    pf3Op,      //   op barrier to op barrier
+    pf3R0,      //   round 0: H0 || H1 || lo0 || lo1
+    pf3WaitRf,  //   merge warps waiting for the refill batch
+    pf3R1,      //   round 1: new root || carried 1
+    pf3WaitC3,  //   merge warps waiting for the level-3 children
+    pf3R2,      //   round 2: new hi1 || carried 2 || H2 || lo2
+    pf3R3,      //   round 3: new hi2 || carried 3 (mailbox) || lo3 write
+    pf3Claim,   //   claim warp: level-3 claim + load
+    pf3Refill,  //   refill warps: go -> refill batch in smem
+    pf3Ctl,     //   control warp: flush + result + lookups
+    pf3Rec,     //   merge leader: last barrier -> record written
+    pf3Wake,    //   record written -> control warp past mb_mdone
+    pf3Post,    //   control warp: record -> op barrier
+    pf3Start,   //   control warp at the op barrier -> round 0 starts
     kNumProf
 };
 
@@ -137,7 +208,7 @@ enum ProfIdx {
 #define BH_WAIT_NOTE(line) ((void)0)
 #define BH_WAIT_NOTE2(slot, w) ((void)0)
 #endif
-constexpr uint32_t kDbgWaitBase = 48;
+constexpr uint32_t kDbgWaitBase = 64;
 
 // Rec: the kernel of BH_FLAG_RECORD heaps (event log); the other kernel
 // carries no recording code at all.
@@ -210,6 +281,18 @@ struct HeapCta {
         asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)::"memory");  // not moved across memory ops
         return c;
     }
+    // per-op timeline of a three-level server (profiling handles): the SM
+    // clock at event `ev` of the hold's op j, for ops [kTlFirst, +kTlOps)
+    // Clocks go to shared memory (sh->tl) and are copied out at the hold's
+    // end: a global store between two clock reads would put its own latency
+    // into the next reading.
+    __device__ __forceinline__ void tl(uint32_t j, uint32_t ev) {
+        if (prof && j - kTlFirst < kTlSmemOps) {
+            unsigned long long c;
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+            sh->tl[(j - kTlFirst) * 24u + ev] = c;
+        }
+    }
     // profile slots go straight to global memory (a red per event, profiling
     // builds only): no per-CTA register array
     __device__ __forceinline__ void pf_add(int idx, unsigned long long v) {
@@ -281,6 +364,8 @@ struct HeapCta {
             // out_pool and status arrays), an insert combiner of a recorded
             // heap too (it logs the waiter's events): words 12-13 name the launch
             st_cg_u64(reinterpret_cast<unsigned long long*>(f + 12), (unsigned long long)rv.ticket);
+            // a servable delete also names its result slot (words 4-5)
+            if (del_req) st_cg_u64(reinterpret_cast<unsigned long long*>(f + 4), rv.ops[cur_op].offset);
             state_store_release(f + (del_req ? 11 : 1), ((uint32_t)t << 1) | 1u);
         }
         const uint32_t granted = (uint32_t)t << 1;
@@ -1303,12 +1388,17 @@ struct HeapCta {
     }
 
     // Leader or kPubLane: is ticket t a delete that posted a serve request?
-    __device__ bool waiting_delete(unsigned long long t, unsigned long long& op) {
+    // The launch, op index and result offset (words 12-13, 2-3, 4-5) load in
+    // one round trip after the request word's acquire.
+    __device__ bool waiting_delete(unsigned long long t, unsigned long long& op, unsigned long long* off = nullptr) {
         uint32_t* f = qline(t);
         if (state_load(f + 11) != (((uint32_t)t << 1) | 1u)) return false;
-        if (ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 12)) != (unsigned long long)rv.ticket)
-            return false;  // a delete of another launch: granted normally
-        op = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 2));
+        const unsigned long long launch = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 12));
+        const unsigned long long o = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 2));
+        const unsigned long long of = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 4));
+        if (launch != (unsigned long long)rv.ticket) return false;  // a delete of another launch: granted normally
+        op = o;
+        if (off) *off = of;
         return true;
     }
 
@@ -1427,16 +1517,20 @@ struct HeapCta {
         // stay out of both groups: the leader's bookkeeping and kPubLane's
         // flush of the previous op + next-waiter lookup run beside them.
         if (threadIdx.x < kRefBase) {
+            // three independent chains on three lanes: the previous op's
+            // releases and hand-off (kPubLane), the next ticket's look-up
+            // (the leader) and the next refill's state word
             if (threadIdx.x == kPubLane) {
                 sv_flush(sh->pd);
-                unsigned long long nop = 0;
-                const bool more = nodes - 1 >= kServeMin && waiting_delete(t + 1, nop);
+            } else if (threadIdx.x == 0) {
+                unsigned long long nop = 0, noff = 0;
+                const bool more = nodes - 1 >= kServeMin && waiting_delete(t + 1, nop, &noff);
                 sh->serve = more;
                 sh->op_next = nop;
-                if (more) {
-                    sh->off_next = rv.ops[nop].offset;
-                    sh->next_w = state_load(st(slot_for_rank(nodes - 1)));  // the next op's refill
-                }
+                sh->off_next = noff;
+            } else if (threadIdx.x == (kPubLane == 1 ? 2u : 1u)) {
+                // the next op's refill (a word of this very slot, or none)
+                sh->next_w = nodes - 1 >= kServeMin ? state_load(st(slot_for_rank(nodes - 1))) : 0xFFFFFFFFu;
             }
         } else if (threadIdx.x < kHalfT) {
             // released here, before the server waits on any claim (below)
@@ -1656,6 +1750,791 @@ struct HeapCta {
         if (hv.variant == BH_BU && leader()) gate_leave(false);
     }
 
+    // ========================================= three-level delete server ==
+    // serve3: delete serving (flat combining of deletes in the root queue
+    // lock, see serve_deletes) with levels 0-2 -- nodes 1-7 -- held in shared
+    // memory, and the work of one op split over warp roles that hand off
+    // through mbarriers instead of CTA-wide barriers:
+    //   warp 0      control: result of the op (the root batch), the previous
+    //               op's level-3 releases and continuation hand-off (one
+    //               fence), look-ups of the next two tickets, refill requests,
+    //               counters and the event log;
+    //   warp 1      claims hi2's children (level 3, the one place the server
+    //               waits on another CTA) and loads them;
+    //   warps 2-13  the merges, in four rounds: H0 || H1 || lo0 || lo1;
+    //               new root || carried 1; new hi1 || carried 2 || H2 || lo2;
+    //               new hi2 || carried 3 (to the next ticket's mailbox) ||
+    //               the lo level-3 child back to HBM;
+    //   warps 14-15 refills, one op each in turn, one op AHEAD: the refill
+    //               source of op j+1 (the last node after op j) is claimed,
+    //               copied, blanked and released while op j is merged.
+    // Every op still runs the reference's delete_min (heap.cpp:411-667):
+    // the same root result, refill source, per-level early stop, elisions,
+    // hi/lo choices (with the tie fix) and counters as heapify_down; levels
+    // 0-2 of op j and the refill of op j+1 touch disjoint nodes (the refill
+    // source is at level >= 5), so running them side by side is equivalent to
+    // running them in order.  The path through levels 0-2 depends only on
+    // the children's batches, so warp 1 knows at the op's start which
+    // level-3 nodes the op needs.  Deadlock freedom as for serve_deletes:
+    // the server waits on other CTAs only in warp 1's level-3 claims and in
+    // the refill warps' claim of the last node; the refill warps hold the
+    // last node only to copy and blank it; the continuation of the previous
+    // op is published by warp 0, which waits on nothing but this CTA's own
+    // merges; across the waits the server holds nodes 1-7, which nobody
+    // waits for while holding anything.
+    static constexpr bool kS3 = Serve3Cfg<Key, K, T>::kOn;
+    static constexpr uint32_t kS3OpThreads = 416;     // warps 0 and 2-13
+    static constexpr uint32_t kS3MergeThreads = 384;  // warps 2-13
+    static constexpr uint32_t kS3BarOp = 5, kS3BarMerge = 6;
+    static constexpr uint32_t kS3MergeLeader = 64;    // lane 0 of warp 2
+    static constexpr uint32_t kVecs = kNodeBytes / 16;
+
+    __device__ __forceinline__ void warp_load_node(Key* s, const Key* g) const {
+        const uint32_t lane = threadIdx.x & 31u;
+        const uint4* gv = reinterpret_cast<const uint4*>(g);
+        uint4* sv = reinterpret_cast<uint4*>(s);
+#pragma unroll 8
+        for (uint32_t i = lane; i < kVecs; i += 32) sv[i] = __ldcg(gv + i);
+    }
+    __device__ __forceinline__ void warp_store_node(Key* g, const Key* s) const {
+        const uint32_t lane = threadIdx.x & 31u;
+        uint4* gv = reinterpret_cast<uint4*>(g);
+        const uint4* sv = reinterpret_cast<const uint4*>(s);
+#pragma unroll 8
+        for (uint32_t i = lane; i < kVecs; i += 32) __stcg(gv + i, sv[i]);
+    }
+    __device__ __forceinline__ void warp_fill_node(Key* g) const {
+        const uint32_t lane = threadIdx.x & 31u;
+        uint4 f;
+        f.x = f.y = f.z = f.w = 0xFFFFFFFFu;
+        uint4* gv = reinterpret_cast<uint4*>(g);
+#pragma unroll 8
+        for (uint32_t i = lane; i < kVecs; i += 32) __stcg(gv + i, f);
+    }
+
+    // hi/lo of two non-empty sibling batches (heap.cpp:628-652, tie fix)
+    __device__ __forceinline__ void s3_children(const Key* L, const Key* R, bool& mc, bool& el, bool& hl) const {
+        if (elide && !needs_merge_full<Key, K>(L, R)) {
+            el = true;
+            mc = false;
+            hl = L[K - 1] <= R[0];
+        } else {
+            el = false;
+            mc = true;
+            hl = !(L[K - 1] > R[K - 1]);
+        }
+    }
+
+    // One warp: acquire_child (heap.cpp:547-585) of both children of `cur`,
+    // lanes 0/1 polling and claiming, the keys loaded by the whole warp in the
+    // claim's round trip.  Returns locked bits (1 = left, 2 = right); rel
+    // states in lrel/rrel (DELMOD for an INSHOLD take-over).
+    // `guess` (lanes 0/1): a claimable word of the child, observed by an
+    // acquire load of this warp after the node's last release or produced by
+    // this CTA's own release (0xFFFFFFFF = none): the first CAS goes out with
+    // it, with no poll before it; a changed word fails the CAS.
+    __device__ uint32_t warp_claim_children(unsigned long long cur, Key* L, Key* R, uint32_t& lrel, uint32_t& rrel,
+                                            uint32_t guess, uint32_t& claimed_w, uint32_t* ntries = nullptr) {
+        const uint32_t lane = threadIdx.x & 31u;
+        uint32_t pending = 3u, locked = 0;
+        lrel = rrel = kAvail;
+        while (pending) {
+            if (ntries) ++*ntries;
+            uint32_t claim = 0, w = 0;
+            const uint32_t gs = sget(guess);
+            if (lane < 2 && ((pending >> lane) & 1u)) {
+                const unsigned long long slot = 2 * cur + lane;
+                if (guess != 0xFFFFFFFFu && (gs == kAvail || gs == kDelMod || gs == kInsHold)) {
+                    claim = 1;
+                    w = guess;
+                } else if (slot <= hv.slot_count) {
+                    uint32_t* p = st(slot);
+                    Backoff b;
+                    for (;;) {
+                        w = state_poll(p);  // relaxed poll + acquire fence (no L1 invalidation per poll)
+                        const uint32_t s = sget(w);
+                        if (s == kAvail || s == kInsHold || s == kDelMod) {
+                            acquire_fence();
+                            claim = 1;
+                            break;
+                        }
+                        if (s == kTarget || s == kMarked) break;  // frozen empty
+                        b.pause();
+                    }
+                }
+            }
+            const uint32_t cl = (__shfl_sync(0xFFFFFFFFu, claim, 0) ? 1u : 0u) |
+                                (__shfl_sync(0xFFFFFFFFu, claim, 1) ? 2u : 0u);
+            uint32_t ok = 0;
+            if (lane < 2 && ((cl >> lane) & 1u)) ok = state_cas_relaxed(st(2 * cur + lane), w, swith(w, kInUse));
+            if (cl & 1u) warp_load_node(L, node(2 * cur));
+            if (cl & 2u) warp_load_node(R, node(2 * cur + 1));
+            const uint32_t okm = (__shfl_sync(0xFFFFFFFFu, ok, 0) ? 1u : 0u) |
+                                 (__shfl_sync(0xFFFFFFFFu, ok, 1) ? 2u : 0u);
+            const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, w, 0), w1 = __shfl_sync(0xFFFFFFFFu, w, 1);
+            if (lane < 2 && ((okm >> lane) & 1u)) rec_lane(kEvAcq, 2 * cur + lane);
+            if (okm & 1u) lrel = sget(w0) == kInsHold ? kDelMod : kAvail;
+            if (okm & 2u) rrel = sget(w1) == kInsHold ? kDelMod : kAvail;
+            if (lane < 2 && ((okm >> lane) & 1u)) claimed_w = swith(w, kInUse);
+            locked |= okm;
+            pending &= ~((pending & ~cl) | okm);  // frozen empty or claimed: done
+            guess = 0xFFFFFFFFu;                  // a failed guess: poll
+        }
+        __syncwarp();
+        return locked;
+    }
+
+    // One warp: refill_root_from(last) (heap.cpp:467-531) into dst, then
+    // arrive on mb (the batch is in shared memory), then blank the last node
+    // and release it.  Never waits while holding the last node.  TD: a
+    // TARGET last node is MARKED and the inserter ships its batch into node 1
+    // in HBM (ship_to_root, heap.cpp:207-216), read from there.
+    // `guess` (lane 0): the last node's word observed by this warp's acquire
+    // load after its last release (0xFFFFFFFF = none): CAS it at once.
+    __device__ void warp_refill(unsigned long long last, Key* dst, unsigned long long* mb, uint32_t guess,
+                                uint32_t jj = ~0u) {
+        const uint32_t lane = threadIdx.x & 31u;
+        uint32_t* p = st(last);
+        for (;;) {
+            uint32_t act = 0, w = 0;
+            const uint32_t gs = sget(guess);
+            if (lane == 0 && guess != 0xFFFFFFFFu && (gs == kAvail || gs == kDelMod || gs == kInsHold)) {
+                act = kTake;
+                w = guess;
+            } else if (lane == 0) {
+                Backoff b;
+                for (;;) {
+                    w = state_poll(p);
+                    const uint32_t s = sget(w);
+                    if (s == kAvail || s == kDelMod || s == kInsHold) {
+                        acquire_fence();
+                        act = kTake;
+                        break;
+                    }
+                    if (s == kTarget && state_cas(p, w, swith(w, kMarked))) {
+                        Backoff wb;
+                        while (sget(state_load(p)) != kAvail) wb.pause();
+                        act = kCoop;
+                        break;
+                    }
+                    b.pause();
+                }
+            }
+            act = __shfl_sync(0xFFFFFFFFu, act, 0);
+            w = __shfl_sync(0xFFFFFFFFu, w, 0);
+            uint32_t ok = 0;
+            if (act == kTake && lane == 0) ok = state_cas_relaxed(p, w, swith(w, kInUse));
+            warp_load_node(dst, node(act == kTake ? last : 1));
+            ok = __shfl_sync(0xFFFFFFFFu, ok, 0);
+            if (act == kCoop) {
+                __syncwarp();
+                if (lane == 0) mb_arrive(mb);
+                return;
+            }
+            guess = 0xFFFFFFFFu;
+            if (!ok) continue;
+            if (lane == 0) rec_lane(kEvAcqRefill, last);
+            __syncwarp();
+            if (lane == 0) {
+                mb_arrive(mb);
+                tl(jj, 16);
+                if (prof && jj - kTlFirst < kTlSmemOps) sh->tl[(jj - kTlFirst) * 24u + 20] = guess != 0xFFFFFFFFu;
+            }
+            warp_fill_node(node(last));
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                rec_lane(kEvRel, last);
+                state_release_relaxed(p, kInUse, sget(w) == kInsHold ? kDelMod : kAvail);
+            }
+            return;
+        }
+    }
+
+    // Claim warp: lanes 0-7 check tickets t0..t0+7 at once (serve_deletes'
+    // waiting_delete: a delete of this launch that posted a serve request,
+    // its op index and result offset from its queue slot line) and note the
+    // confirmed ones in the look-ahead ring; one batch of two round trips
+    // covers the next several ops.
+    __device__ void s3_lookahead(unsigned long long t0) {
+        Sv3Shared& s3 = sh->s3;
+        const uint32_t lane = threadIdx.x & 31u;
+        if (lane < 8) {
+            const unsigned long long x = t0 + lane;
+            if (s3.la_tk[x & 7u] != x) {
+                uint32_t* f = qline(x);
+                // relaxed poll, acquire fence only on a match (acquire loads
+                // invalidate L1 and stall the merge warps' shared memory work)
+                if (state_poll(f + 11) == (((uint32_t)x << 1) | 1u)) {
+                    acquire_fence();
+                    const unsigned long long launch = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 12));
+                    const unsigned long long o = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 2));
+                    const unsigned long long of = ld_cg_u64(reinterpret_cast<const unsigned long long*>(f + 4));
+                    if (launch == (unsigned long long)rv.ticket) {
+                        s3.la_op[x & 7u] = o;
+                        s3.la_off[x & 7u] = of;
+                        __threadfence_block();
+                        *reinterpret_cast<volatile unsigned long long*>(&s3.la_tk[x & 7u]) = x;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    __device__ __forceinline__ bool s3_have(unsigned long long x) const {
+        const bool y = *reinterpret_cast<volatile const unsigned long long*>(&sh->s3.la_tk[x & 7u]) == x;
+        __threadfence_block();  // the entry's op/offset were written before its tag
+        return y;
+    }
+
+    // Warp 1 of a three-level server: per op, claims hi2's children (level 3)
+    // on the merge leader's request (sent one op ahead); in between, looks
+    // ahead in the root queue for the next waiting deletes (the ring).  A
+    // claim first CASes the word the server's own release of the node
+    // produced (the data is then the server's own), else polls.
+    __device__ void s3_claim_loop() {
+        Sv3Shared& s3 = sh->s3;
+        const uint32_t lane = threadIdx.x & 31u;
+        unsigned long long t = sh->root_tk;
+        for (uint32_t n = 0;; ++n) {
+            for (;;) {
+                if (__shfl_sync(0xFFFFFFFFu, (uint32_t)mb_test(&s3.mb_go3, n & 1u), 0)) break;
+                bool need = false;
+                if (lane < 8) need = s3.la_tk[(t + 1 + lane) & 7u] != t + 1 + lane;
+                if (__any_sync(0xFFFFFFFFu, need)) s3_lookahead(t + 1);
+                __nanosleep(64);
+            }
+            const uint32_t hi2 = s3.g3_hi2;
+            if (!hi2) break;
+            const unsigned long long tc = now();
+            t = s3.g3_t;
+            cur_op = s3.g3_op;
+            const uint32_t jj = s3.g3_j;
+            if (lane == 0) tl(jj, 13);
+            const uint32_t bL = s3.g3_L, bR = s3.g3_R;
+            const uint32_t i0 = 2u * hi2 - 8u;
+            uint32_t guess = 0xFFFFFFFFu, lrel, rrel, cw = 0, ntries = 0;
+            if (lane < 2) guess = s3.w3pred[i0 + lane];
+            const uint32_t lk = warp_claim_children(hi2, buf(bL), buf(bR), lrel, rrel, guess, cw, &ntries);
+            if (lane < 2 && ((lk >> lane) & 1u)) s3.w3in[i0 + lane] = cw;
+            __syncwarp();
+            if (lane == 0) {
+                s3.lk3 = lk & 1u;
+                s3.rk3 = lk >> 1;
+                s3.lrel3 = lrel;
+                s3.rrel3 = rrel;
+                mb_arrive(&s3.mb_c3);
+                tl(jj, 14);
+                if (prof && jj - kTlFirst < kTlSmemOps) sh->tl[(jj - kTlFirst) * 24u + 18] = ntries;
+            }
+            if (prof && lane == 0) atomicAdd(&hv.prof[pf3Claim], now() - tc);
+        }
+    }
+
+    // Root held (ticket sh->root_tk), gate passed, buf(0) = root batch,
+    // partial buffer empty, >= kServeMin nodes, the next ticket a waiting
+    // delete of this launch.
+    __device__ void serve3(unsigned long long opi, unsigned long long seq, unsigned long long nodes) {
+        Sv3Shared& s3 = sh->s3;
+        const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+        if (threadIdx.x == 0) {
+            mb_init(&s3.mb_go[0], 1);
+            mb_init(&s3.mb_go[1], 1);
+            mb_init(&s3.mb_rf[0], 1);
+            mb_init(&s3.mb_rf[1], 1);
+            mb_init(&s3.mb_c3, 1);
+            mb_init(&s3.mb_go3, 1);
+            mb_init(&s3.mb_rec, 1);
+        }
+        // ---- hold start: nodes 2..7 into buffers 1..6 (root in buffer 0)
+        uint32_t delmod = 0, okall;
+        acquire_children(1, buf(1), buf(2));
+        okall = sh->lk & sh->rk;
+        delmod |= (sh->lrel == kDelMod ? 1u << 2 : 0u) | (sh->rrel == kDelMod ? 1u << 3 : 0u);
+        __syncthreads();
+        acquire_children(2, buf(3), buf(4));
+        okall &= sh->lk & sh->rk;
+        delmod |= (sh->lrel == kDelMod ? 1u << 4 : 0u) | (sh->rrel == kDelMod ? 1u << 5 : 0u);
+        __syncthreads();
+        acquire_children(3, buf(5), buf(6));
+        okall &= sh->lk & sh->rk;
+        delmod |= (sh->lrel == kDelMod ? 1u << 6 : 0u) | (sh->rrel == kDelMod ? 1u << 7 : 0u);
+        if (threadIdx.x == 0) {
+            if (!okall) atomicOr(&hdr->error_flags, (unsigned long long)kErrInteriorEmpty);
+            s3.w0_done = 0;
+            s3.w0_seen = 0;
+            if (prof)
+                for (uint32_t i = 0; i < kTlSmemOps * 24u; ++i) sh->tl[i] = 0;
+            for (int i = 0; i < 8; ++i) {
+                s3.la_tk[i] = ~0ull;
+                s3.w3pred[i] = 0xFFFFFFFFu;
+            }
+        }
+        __syncthreads();
+
+        if (warp >= 14) {
+            // ---- refill warps: one op each in turn
+            // (each warp observes its next source -- two ranks lower -- once
+            // its refill is done, so the next claim needs no poll)
+            const uint32_t g = warp - 14;
+            unsigned long long pre_rank = 0;
+            uint32_t pre_w = 0xFFFFFFFFu;
+            for (uint32_t n = 0;; ++n) {
+                // idle until the next request: test + sleep (a try_wait spin
+                // would take issue slots from the merge warps of its SMSP)
+                while (__shfl_sync(0xFFFFFFFFu, (uint32_t)mb_test(&s3.mb_go[g], n & 1u), 0) == 0) __nanosleep(100);
+                const unsigned long long rank = s3.go_last[g];
+                if (!rank) break;
+                const uint32_t b = s3.go_buf[g];
+                const uint32_t jj = s3.go_j[g];
+                cur_op = s3.go_op[g];
+                const unsigned long long tr = now();
+                if (lane == 0) tl(jj, 15);
+                warp_refill(slot_for_rank(rank), buf(b), &s3.mb_rf[g], rank == pre_rank ? pre_w : 0xFFFFFFFFu, jj);
+                if (lane == 0) tl(jj, 17);
+                if (prof && lane == 0) atomicAdd(&hv.prof[pf3Refill], now() - tr);
+                pre_rank = rank > 2 ? rank - 2 : 0;
+                if (lane == 0 && pre_rank) pre_w = state_load(st(slot_for_rank(pre_rank)));
+            }
+        } else if (warp == 1) {
+            s3_claim_loop();
+        } else if (warp == 0) {
+            s3_control_loop();
+        } else {
+            s3_merge_loop(opi, seq, nodes);
+        }
+        __syncthreads();
+
+        if (prof)  // the timeline (first hold of the run only)
+            for (uint32_t i = threadIdx.x; i < kTlSmemOps * 24u; i += T)
+                if (sh->tl[i]) atomicCAS(&hv.prof[kTlBase + (i / 24u) * 32u + i % 24u], 0ull, sh->tl[i]);
+        // ---- hold end: write the top levels back, release them, the last
+        // op's level-3 nodes and the root; run its continuation here
+        const Sv3Rec& R = s3.rec[(s3.w0_done - 1u) & 3u];
+        const unsigned long long t = R.t;
+        const unsigned long long lastop = R.op;
+        nodes = sh->nodes;
+        seq = R.seq + 1;
+        for (int i = 1; i <= 7; ++i) cta_store<Key, T>(node(i), buf(s3.nb_end[i]), K);
+        if (leader()) {
+            st_cg_u64(&hdr->node_count, nodes);
+            st_cg_u64(&hdr->delete_count, seq);
+        }
+        __syncthreads();
+        if (leader()) {
+            for (uint32_t i = 0; i < R.nrel; ++i) rec_for(lastop, kEvRel, R.relslot[i]);
+            __threadfence();
+            for (uint32_t i = 2; i <= 7; ++i) state_release_relaxed(st(i), kInUse, ((delmod >> i) & 1u) ? kDelMod : kAvail);
+            for (uint32_t i = 0; i < R.nrel; ++i) state_release_relaxed(st(R.relslot[i]), kInUse, R.relst[i]);
+            state_store_relaxed(qline(t + 1), (uint32_t)(t + 1) << 1);  // root_unlock
+        }
+        cur_op = lastop;
+        const unsigned long long cont = R.cont;
+        const uint32_t crel = R.crel;
+        // the carried batch of the last op's continuation: in shared memory,
+        // or in the mailbox of ticket t+1 (no one else reads that slot)
+        int cb = (int)R.c3buf;
+        if (cont && R.c3buf == 0xFFFFFFFFu) {
+            cb = 23;
+            cta_load<Key, T>(buf(cb), mbox(t + 1), K);
+        }
+        __syncthreads();
+        if (cont) heapify_down(cb, 0, false, cont, crel);
+        rec(kEvRes, 0);
+        if (hv.variant == BH_BU && leader()) gate_leave(false);
+    }
+
+    // Control warp (warp 0) of a three-level server, one op behind the
+    // merges: for each op record (in op order): the result (the root batch
+    // before the op), then the hand-off of the op's continuation to the CTA of
+    // the next ticket (carried batch into its mailbox if still in shared
+    // memory, one fence, the op's level-3 releases, the served flag with the
+    // continuation word).  Never waits on another CTA.
+    __device__ void s3_control_loop() {
+        Sv3Shared& s3 = sh->s3;
+        const uint32_t lane = threadIdx.x & 31u;
+        for (uint32_t j = 0;; ++j) {
+            while (__shfl_sync(0xFFFFFFFFu, (uint32_t)mb_test(&s3.mb_rec, j & 1u), 0) == 0) __nanosleep(32);
+            const unsigned long long tc = now();
+            if (lane == 0) {
+                tl(j, 11);
+                s3.w0_seen = j + 1;
+            }
+            const Sv3Rec& R = s3.rec[j & 3u];
+            warp_store_node(static_cast<Key*>(rv.out_pool) + R.off, buf(R.rootbuf));
+            if (lane == 0 && buf(R.rootbuf)[K - 1] == kMaxKey)
+                atomicOr(&hdr->error_flags, (unsigned long long)kErrSentinelEscaped);
+            status(R.op, BH_OK, K, R.seq);
+            count(cDeletes);
+            count(cMerges, R.cnt_merges);
+            count(cElided, R.cnt_elided);
+            count(cEarlyStops, R.cnt_early);
+            count(cVisits, R.cnt_visits);
+            if (!R.last) {
+                if (R.cont && R.c3buf != 0xFFFFFFFFu) warp_store_node(mbox(R.t + 1), buf(R.c3buf));
+                __syncwarp();
+                if (lane == 0) {
+                    const unsigned long long pub = R.t + 1;
+                    if (record) {
+                        for (uint32_t i = 0; i < R.nrel; ++i) rec_for(R.op, kEvRel, R.relslot[i]);
+                        st_cg_u64(reinterpret_cast<unsigned long long*>(qline(pub) + 14), R.op);
+                    }
+                    __threadfence();  // the mailbox batch, the released nodes' keys, word 14
+                    for (uint32_t i = 0; i < R.nrel; ++i) state_release_relaxed(st(R.relslot[i]), kInUse, R.relst[i]);
+                    if (hv.variant == BH_BU) atomicAdd(&hdr->deleters, 1ull);  // op j+1 is in the delete phase
+                    const uint32_t pubw = (uint32_t)R.cont | (R.crel == kDelMod ? 0x80000000u : 0u);
+                    const unsigned long long w = ((unsigned long long)pubw << 32) | (((uint32_t)pub << 1) | 1u);
+                    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(qline(pub)), "l"(w) : "memory");
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                tl(j, 12);
+                s3.w0_done = j + 1;
+            }
+            if (prof && lane == 0) atomicAdd(&hv.prof[pf3Ctl], now() - tc);
+            if (R.last) break;
+        }
+    }
+
+    // Warps 2-13 of a three-level server: the op loop.  Every merge thread
+    // computes the same decisions, node map and buffer plan; the merge leader
+    // sends the requests (level-3 claim, refills), writes the records and
+    // decides whether the hold goes on.  Per op, after the refill batch is in:
+    //   fast path (no merge of a carried batch at levels 0-1: the refill
+    //   batch moves down unchanged, the usual case): round A H0 || lo0 || H1,
+    //   round B lo1 || H2 || lo2 (to HBM) once the level-3 children are in,
+    //   round C new hi2 || carried 3 only when the refill interleaves H2;
+    //   general path: the four rounds of serve_deletes' schedule, one level
+    //   deeper.
+    // Every merge runs through one inlined call site (instruction cache).
+    __device__ void s3_merge_loop(unsigned long long op, unsigned long long seq, unsigned long long nodes) {
+        Sv3Shared& s3 = sh->s3;
+        const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+        const uint32_t mw = warp - 2u, grp = mw >> 2, gw = mw & 3u;
+        const bool ml = threadIdx.x == kS3MergeLeader;
+        unsigned long long t = sh->root_tk;
+        unsigned long long off = rv.ops[op].offset;
+        // node map: 5 bits per node 1..7 (buffer index)
+        unsigned long long nbp = 0;
+        for (uint32_t i = 1; i <= 7; ++i) nbp |= (unsigned long long)(i - 1) << (5 * i);
+        auto nbg = [&](uint32_t i) { return (uint32_t)(nbp >> (5 * i)) & 31u; };
+        auto nbs = [&](uint32_t i, uint32_t b) {
+            nbp = (nbp & ~(31ull << (5 * i))) | ((unsigned long long)b << (5 * i));
+        };
+        uint32_t rfb = 7;                           // this op's refill buffer
+        uint32_t resv = 0;                          // reserved for the control warp (previous op)
+        bool req_next = false;                      // refill of op j+1 requested
+        for (uint32_t j = 0;; ++j) {
+            const unsigned long long t_op = now();
+            // ---- buffer plan: the control warp must be done with op j-2
+            if (j >= 2)
+                while (s3.w0_done < j - 1) __nanosleep(20);
+            uint32_t used = resv | (1u << rfb);
+            for (uint32_t i = 1; i <= 7; ++i) used |= 1u << nbg(i);
+            const uint32_t fr = ~used & 0xFFFFFFu;
+            // the k-th free buffer: lane L holds buffer L's rank among the free ones
+            const uint32_t myrank = __popc(fr & ((1u << lane) - 1u));
+            const bool myfree = lane < 24 && ((fr >> lane) & 1u);
+            auto scratch = [&](uint32_t k) {
+                return (uint32_t)__ffs(__ballot_sync(0xFFFFFFFFu, myfree && myrank == k)) - 1u;
+            };
+            const uint32_t bH0 = scratch(0), blo0 = scratch(1), bH1 = scratch(2), blo1 = scratch(3),
+                           bL3 = scratch(4), bR3 = scratch(5), bH2 = scratch(6), bnr = scratch(7), bc1 = scratch(8),
+                           bnh1 = scratch(9), bc2 = scratch(10), bnh2 = scratch(11), brfn = scratch(12);
+            // ---- the path through levels 0-1 (children batches only)
+            bool mc0, el0, hl0, mc1, el1, hl1;
+            const uint32_t nb2 = nbg(2), nb3 = nbg(3);
+            const Key* n2 = buf(nb2);
+            const Key* n3 = buf(nb3);
+            s3_children(n2, n3, mc0, el0, hl0);
+            const uint32_t hi1 = hl0 ? 2u : 3u, lo1 = hi1 ^ 1u;
+            const Key* k1l = buf(nbg(2 * hi1));
+            const Key* k1r = buf(nbg(2 * hi1 + 1));
+            s3_children(k1l, k1r, mc1, el1, hl1);
+            const uint32_t hi2 = hl1 ? 2u * hi1 : 2u * hi1 + 1u, lo2 = hi2 ^ 1u;
+            if (ml) {
+                tl(j, 0);
+                // the claim warp: hi2's children
+                s3.g3_t = t;
+                s3.g3_op = op;
+                s3.g3_j = j;
+                s3.g3_hi2 = hi2;
+                s3.g3_L = bL3;
+                s3.g3_R = bR3;
+                mb_arrive(&s3.mb_go3);
+                if (j == 0) s3_go(0, nodes, rfb, op);  // the first refill is not ahead
+                req_next = false;
+                if (nodes - 1 >= kServeMin && s3_have(t + 1)) {
+                    s3_go(j + 1, nodes - 1, brfn, s3.la_op[(t + 1) & 7u]);
+                    req_next = true;
+                }
+            }
+            // ---- level-0/1 bounds: the largest key of H0' and H1' (the k
+            // smallest of the children), without merging
+            const Key h0max = mc0 ? warp_kth_max<Key, K>(n2, n3) : (hl0 ? n2 : n3)[K - 1];
+            const Key h1max = mc1 ? warp_kth_max<Key, K>(k1l, k1r) : (hl1 ? k1l : k1r)[K - 1];
+            mb_wait(&s3.mb_rf[j & 1u], (j >> 1) & 1u);
+            if (ml) tl(j, 2);
+            const Key* RF = buf(rfb);
+            const Key rmin = RF[0], rmax = RF[K - 1];
+            const bool stop0 = rmax <= n2[0] && rmax <= n3[0];
+            const bool mcur0 = !stop0 && !(elide && h0max <= rmin);  // H0'.min < refill.max: H0' <= refill is the test
+            const bool stop1 = !stop0 && !mcur0 && rmax <= k1l[0] && rmax <= k1r[0];
+            const bool mcur1f = !stop0 && !mcur0 && !stop1 && !(elide && h1max <= rmin);
+            const bool fast = !stop0 && !mcur0 && !stop1 && !mcur1f;
+            // decisions filled in below
+            bool stop1g = stop1, mcur1 = false, stop2 = false, early2 = false, go2 = false, mcur2 = false;
+            bool mc2 = false, el2 = false, hl2 = false;
+            uint32_t lk3 = 0, rk3 = 0, lrel3 = kAvail, rrel3 = kAvail;
+            uint32_t c1b = rfb, c2b = rfb;
+            const uint32_t bH0p = mc0 ? bH0 : nbg(hi1);
+            const uint32_t bH1p = mc1 ? bH1 : nbg(hi2);
+            uint32_t bH2p = 0;
+            bool c3_mbox = false;
+            const uint32_t nrounds_max = fast ? 3u : 4u;
+#pragma unroll 1
+            for (uint32_t r = 0; r < nrounds_max; ++r) {
+                const Key* A = nullptr;
+                const Key* B = nullptr;
+                Key* out = nullptr;
+                bool second = false, global = false, act = false, copy = false;
+                if (r == 0) {  // H0 || lo0 || H1 (both paths)
+                    if (grp == 0) { act = mc0; A = n2; B = n3; out = buf(bH0); }
+                    else if (grp == 1) { act = mc0; A = n2; B = n3; out = buf(blo0); second = true; }
+                    else { act = mc1; A = k1l; B = k1r; out = buf(bH1); }
+                } else if (fast || r >= 2) {
+                    // level 2 decisions need the level-3 children (and, on the
+                    // general path, carried 2 from round 2)
+                    if ((fast && r == 1) || (!fast && r == 2)) {
+                        mb_wait(&s3.mb_c3, j & 1u);
+                        if (ml) tl(j, 4);
+                        lk3 = s3.lk3;
+                        rk3 = s3.rk3;
+                        lrel3 = s3.lrel3;
+                        rrel3 = s3.rrel3;
+                        const Key* L3 = buf(bL3);
+                        const Key* R3 = buf(bR3);
+                        const bool le3 = !lk3 || L3[0] == kMaxKey, re3 = !rk3 || R3[0] == kMaxKey;
+                        if (!le3 && !re3) s3_children(L3, R3, mc2, el2, hl2);
+                        else hl2 = !le3;
+                    }
+                    const Key* L3 = buf(bL3);
+                    const Key* R3 = buf(bR3);
+                    if (fast && r == 1) {  // lo1 || H2 || lo2 -> HBM; level 2 with the refill
+                        const bool le3 = !lk3 || L3[0] == kMaxKey, re3 = !rk3 || R3[0] == kMaxKey;
+                        stop2 = le3 && re3;
+                        if (!stop2 && rmax <= (le3 ? kMaxKey : L3[0]) && rmax <= (re3 ? kMaxKey : R3[0])) {
+                            early2 = true;
+                            stop2 = true;
+                        }
+                        go2 = !stop2;
+                        c2b = rfb;
+                        bH2p = mc2 ? bH2 : (hl2 ? bL3 : bR3);
+                        // H2' (the k smallest of the level-3 children) bounds the
+                        // refill's last step without merging first
+                        const Key h2max = mc2 ? warp_kth_max<Key, K>(L3, R3) : buf(bH2p)[K - 1];
+                        mcur2 = go2 && !(elide && h2max <= rmin);
+                        if (grp == 0) { act = mc1; A = k1l; B = k1r; out = buf(blo1); second = true; }
+                        else if (grp == 1) { act = go2 && mc2; A = L3; B = R3; out = buf(bH2); }
+                        else {
+                            act = go2 && mc2; A = L3; B = R3; second = true; global = true;
+                            out = node(hl2 ? 2ull * hi2 + 1 : 2ull * hi2);
+                        }
+                    } else if (fast && r == 2) {  // only if the refill interleaves H2'
+                        c3_mbox = true;
+                        if (grp == 0) { act = true; A = RF; B = buf(bH2p); out = buf(bnh2); }
+                        else if (grp == 1) { act = true; A = RF; B = buf(bH2p); out = mbox(t + 1); second = true; global = true; }
+                    } else if (r == 2) {  // general: level 1 with carried 1 || H2
+                        const Key* C1 = buf(c1b);
+                        stop1g = !stop0 && C1[K - 1] <= k1l[0] && C1[K - 1] <= k1r[0];
+                        const bool go1 = !stop0 && !stop1g;
+                        mcur1 = go1 && !(elide && !needs_merge_full<Key, K>(C1, buf(bH1p)));
+                        c2b = mcur1 ? bc2 : c1b;
+                        if (grp == 2) { act = go1 && mc2; A = L3; B = R3; out = buf(bH2); }
+                        else { act = mcur1; A = C1; B = buf(bH1p); out = buf(grp == 0 ? bnh1 : bc2); second = grp == 1; }
+                    } else {  // general r == 3: level 2 with carried 2 || lo2 -> HBM
+                        const bool go1 = !stop0 && !stop1g;
+                        const bool le3 = !lk3 || L3[0] == kMaxKey, re3 = !rk3 || R3[0] == kMaxKey;
+                        const Key* C2 = buf(c2b);
+                        if (go1) {
+                            stop2 = le3 && re3;
+                            if (!stop2 && C2[K - 1] <= (le3 ? kMaxKey : L3[0]) && C2[K - 1] <= (re3 ? kMaxKey : R3[0])) {
+                                early2 = true;
+                                stop2 = true;
+                            }
+                        }
+                        go2 = go1 && !stop2;
+                        bH2p = mc2 ? bH2 : (hl2 ? bL3 : bR3);
+                        mcur2 = go2 && !(elide && !needs_merge_full<Key, K>(C2, buf(bH2p)));
+                        c3_mbox = mcur2;
+                        if (grp == 0) { act = mcur2; A = C2; B = buf(bH2p); out = buf(bnh2); }
+                        else if (grp == 1) { act = mcur2; A = C2; B = buf(bH2p); out = mbox(t + 1); second = true; global = true; }
+                        else {
+                            act = go2 && mc2; A = L3; B = R3; second = true; global = true;
+                            out = node(hl2 ? 2ull * hi2 + 1 : 2ull * hi2);
+                        }
+                    }
+                } else {  // general r == 1: level 0 with the refill || lo1
+                    c1b = mcur0 ? bc1 : rfb;
+                    if (grp == 2) { act = mc1; A = k1l; B = k1r; out = buf(blo1); second = true; }
+                    else { act = mcur0; A = RF; B = buf(bH0p); out = buf(grp == 0 ? bnr : bc1); second = grp == 1; }
+                }
+                if (act)
+                    grp_merge_half_rt<Key, K, 4>(A, B, out, gw, second, global);
+                else if (copy)
+                    grp_store<Key>(out, A, K, threadIdx.x & 127u, 128u);
+                if (r == 0 && (threadIdx.x & 127u) == 64u) tl(j, 8u + grp);  // group leaders: merge done
+                // the leader decides, before the op's last barrier, whether
+                // the hold goes on (every merge thread reads it after)
+                const bool last_round = fast ? (r == 2 || (r == 1 && !mcur2)) : r == 3;
+                if (ml && last_round) {
+                    const bool on = nodes - 1 >= kServeMin && s3_have(t + 1);
+                    s3.hold_on[j & 1u] = on;
+                    if (on) {
+                        s3.nx_op[j & 1u] = s3.la_op[(t + 1) & 7u];
+                        s3.nx_off[j & 1u] = s3.la_off[(t + 1) & 7u];
+                        if (!req_next) {
+                            s3_go(j + 1, nodes - 1, brfn, s3.la_op[(t + 1) & 7u]);
+                            req_next = true;
+                        }
+                    }
+                }
+                grp_sync(kS3BarMerge, kS3MergeThreads);
+                if (ml) tl(j, r == 0 ? 1 : r == 1 ? 3 : r == 2 ? 5 : 6);
+                if (last_round) break;
+            }
+            // ---- the op's node map, record and counters
+            const uint32_t rootb = nbg(1);
+            uint32_t c3buf = 0xFFFFFFFFu;
+            unsigned long long cont = 0;
+            uint32_t crel = kAvail;
+            const uint32_t nrb = stop0 ? rfb : (mcur0 ? bnr : bH0p);
+            const uint32_t nh1b = mcur1 ? bnh1 : bH1p;
+            const bool go1 = !stop0 && !(fast ? stop1 : stop1g);
+            nbs(1, nrb);
+            if (!stop0) {
+                if (mc0) nbs(lo1, blo0);
+                nbs(hi1, go1 ? (fast ? bH1p : nh1b) : c1b);
+                if (go1) {
+                    if (mc1) nbs(lo2, blo1);
+                    nbs(hi2, stop2 ? c2b : (mcur2 ? bnh2 : bH2p));
+                }
+            }
+            const unsigned long long hi3 = hl2 ? 2ull * hi2 : 2ull * hi2 + 1, lo3 = hi3 ^ 1ull;
+            if (go2) {
+                cont = hi3;
+                crel = hl2 ? lrel3 : rrel3;
+                if (!c3_mbox) c3buf = c2b;  // the carried batch moves down unchanged
+            }
+            const bool on = s3.hold_on[j & 1u] != 0;
+            if (ml) {
+                Sv3Rec& R = s3.rec[j & 3u];
+                uint32_t merges = 0, elided = 0, early = 0, visits = 0;
+                if (stop0) {
+                    ++early;
+                } else {
+                    merges += mc0 + mcur0;
+                    elided += el0 + !mcur0;
+                    ++visits;
+                    if (!go1) {
+                        ++early;
+                    } else {
+                        merges += mc1 + mcur1;
+                        elided += el1 + !mcur1;
+                        ++visits;
+                        if (stop2) {
+                            early += early2;
+                        } else {
+                            merges += mc2 + mcur2;
+                            elided += el2 + !mcur2;
+                            ++visits;
+                        }
+                    }
+                }
+                R.op = op;
+                R.off = off;
+                R.seq = seq;
+                R.t = t;
+                R.cont = cont;
+                R.crel = crel;
+                R.rootbuf = rootb;
+                R.c3buf = c3buf;
+                R.cnt_merges = merges;
+                R.cnt_elided = elided;
+                R.cnt_early = early;
+                R.cnt_visits = visits;
+                R.last = !on;
+                uint32_t nrel = 0;
+                if (go2) {
+                    if (hl2 ? rk3 : lk3) {
+                        R.relslot[0] = lo3;
+                        R.relst[0] = hl2 ? rrel3 : lrel3;
+                        nrel = 1;
+                    }
+                } else {
+                    if (lk3) {
+                        R.relslot[nrel] = 2ull * hi2;
+                        R.relst[nrel++] = lrel3;
+                    }
+                    if (rk3) {
+                        R.relslot[nrel] = 2ull * hi2 + 1;
+                        R.relst[nrel++] = rrel3;
+                    }
+                }
+                R.nrel = nrel;
+                // the words the control warp's releases will produce: the next
+                // claims of these nodes CAS them directly
+                for (uint32_t i = 0; i < nrel; ++i) {
+                    const uint32_t x = (uint32_t)R.relslot[i] - 8u;
+                    s3.w3pred[x] = s3.w3in[x] + 8u + R.relst[i] - kInUse;
+                }
+                if (cont) s3.w3pred[(uint32_t)cont - 8u] = 0xFFFFFFFFu;
+                if (record) {  // the op's turn at nodes 1-7 ends; the next op's begins
+                    for (unsigned long long i = 1; i <= 7; ++i) rec_for(op, kEvRel, i);
+                    if (on)
+                        for (unsigned long long i = 1; i <= 7; ++i) rec_for(s3.nx_op[j & 1u], kEvAcq, i);
+                }
+                if (prof) {
+                    atomicAdd(&hv.prof[pf3Ops], 1ull);
+                    atomicAdd(&hv.prof[pf3Op], now() - t_op);
+                    atomicAdd(&hv.prof[fast ? pf3R0 : pf3R1], 1ull);
+                }
+                // one record phase at a time: the control warp has taken the last one
+                while (s3.w0_seen < j) __nanosleep(20);
+                mb_arrive(&s3.mb_rec);
+            }
+            resv = (1u << rootb) | (c3buf != 0xFFFFFFFFu ? 1u << c3buf : 0u);
+            rfb = brfn;
+            if (!on) {
+                if (ml) {  // the refill and claim warps leave; hold-end state
+                    s3_go(j + 1, 0, 0, 0);
+                    s3_go(j + 2, 0, 0, 0);
+                    s3.g3_hi2 = 0;
+                    mb_arrive(&s3.mb_go3);
+                    for (uint32_t i = 1; i <= 7; ++i) s3.nb_end[i] = nbg(i);
+                    sh->nodes = nodes - 1;
+                }
+                break;
+            }
+            ++t;
+            op = s3.nx_op[j & 1u];
+            off = s3.nx_off[j & 1u];
+            ++seq;
+            --nodes;
+        }
+    }
+
+    // Merge leader: a refill request for op j (rank 0 = leave the loop).
+    __device__ void s3_go(uint32_t j, unsigned long long rank, uint32_t b, unsigned long long op) {
+        Sv3Shared& s3 = sh->s3;
+        s3.go_last[j & 1u] = rank;
+        s3.go_j[j & 1u] = j;
+        s3.go_buf[j & 1u] = b;
+        s3.go_op[j & 1u] = op;
+        mb_arrive(&s3.mb_go[j & 1u]);
+    }
+
     __device__ void do_delete(unsigned long long opi, const bh_op& o) {
         const unsigned long long t0 = now();
         rec(kEvInv, 0);
@@ -1779,6 +2658,12 @@ struct HeapCta {
             }
             __syncthreads();
             if (sh->serve) {
+                if constexpr (kS3) {
+                    if (hv.flags & kDbgServe3) {
+                        serve3(opi, seq, nodes);
+                        return;
+                    }
+                }
                 serve_deletes(opi, seq, nodes);
                 return;
             }
@@ -2069,7 +2954,8 @@ template <typename Key, int K>
 struct KernelCfg {
     static constexpr int kWant = K / BH_THREADS_DIV;
     static constexpr int kThreads = kWant < 32 ? 32 : (kWant > BH_THREADS_CAP ? BH_THREADS_CAP : kWant);
-    static constexpr uint32_t kSmem = 10u * K * sizeof(Key) + 64;  // + window over-read pad
+    // 10 node buffers, 24 where the three-level delete server runs; + window over-read pad
+    static constexpr uint32_t kSmem = (Serve3Cfg<Key, K, kThreads>::kOn ? 24u : 10u) * K * sizeof(Key) + 64;
 };
 
 }  // namespace bh

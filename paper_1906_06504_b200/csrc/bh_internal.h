@@ -24,7 +24,10 @@ constexpr uint32_t kStateStride = 8;  // uint32 words
 constexpr uint32_t kRootQueue = 4096;
 constexpr uint32_t kRootFlagStride = 32;  // uint32 words
 // Profile buffer: 48 counters + 4 debug words per CTA (up to 4096 CTAs).
-constexpr uint32_t kProfWords = 48 + 4 * 4096;
+// profile words: counters (64), per-CTA wait notes (4 x 4096), then a
+// per-op event timeline of a three-level server (kTlOps ops x 32 clocks)
+constexpr uint32_t kTlBase = 64 + 4 * 4096, kTlFirst = 1000, kTlOps = 64;
+constexpr uint32_t kProfWords = kTlBase + kTlOps * 32;
 
 // Debug-only protocol toggles (bh_create flags, not in the public header).
 constexpr uint32_t kDbgSeqRefill = 0x100;       // reference refill order in every delete
@@ -33,6 +36,7 @@ constexpr uint32_t kDbgSerialLanes = 0x400;     // claim children one after the 
 constexpr uint32_t kDbgNoCombine = 0x800;       // no insert combining in the root queue lock
 constexpr uint32_t kDbgParkClimb = 0x1000;      // reference BU climb (fenced park, reload on re-take)
 constexpr uint32_t kDbgNoDelServe = 0x2000;     // no delete serving in the root queue lock
+constexpr uint32_t kDbgServe3 = 0x4000;         // three-level delete server (experimental, DESIGN.md s.6) where it fits
 
 // Heap header, root-lock guarded (reference heap.hpp:173-177).  One cache
 // line; the partial buffer follows in its own allocation.

@@ -221,6 +221,132 @@ __device__ __noinline__ void warp_half_bt(const Key* __restrict__ A, const Key* 
     }
 }
 
+// The same network inlined (no call: the caller's live registers are not
+// saved to the stack around it), for the three-level delete server's merges.
+template <typename Key, int K, int E, bool Global>
+__device__ __forceinline__ void warp_half_bt_inl(const Key* __restrict__ A, const Key* __restrict__ B,
+                                             Key* __restrict__ out, uint32_t D) {
+    constexpr uint32_t W = 32u * E;
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t lo = D > (uint32_t)K ? D - K : 0u;
+    uint32_t hi = D < (uint32_t)K ? D : (uint32_t)K;
+#pragma unroll
+    for (uint32_t span = (uint32_t)K; span > 0; span >>= 5) {
+        const uint32_t g = span > 32 ? ((span + 31u) >> 5) | 1u : 1u;
+        const uint32_t p = lo + (lane + 1u) * g;
+        const bool ok = p <= hi && A[p - 1] <= B[D - p];
+        lo += (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, ok)) * g;
+        const uint32_t h2 = lo + g - 1u;
+        hi = h2 < hi ? h2 : hi;
+        if (g == 1u) break;
+    }
+    const uint32_t a = lo, b = D - lo;
+    Key v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const uint32_t i = e * 32u + lane;
+        const Key x = a + i < (uint32_t)K ? A[a + i] : KeyLimits<Key>::kMax;
+        const uint32_t j = b + (W - 1u - i);
+        const Key y = j < (uint32_t)K ? B[j] : KeyLimits<Key>::kMax;
+        v[e] = x < y ? x : y;
+    }
+#pragma unroll
+    for (int rs = E / 2; rs >= 1; rs >>= 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e & rs) == 0) {
+                const Key x = v[e], y = v[e + rs];
+                v[e] = x < y ? x : y;
+                v[e + rs] = x < y ? y : x;
+            }
+        }
+    }
+#pragma unroll
+    for (int ls = 16; ls >= 1; ls >>= 1) {
+        const bool upper = (lane & (uint32_t)ls) != 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const Key o = __shfl_xor_sync(0xFFFFFFFFu, v[e], ls);
+            v[e] = upper ? (v[e] < o ? o : v[e]) : (v[e] < o ? v[e] : o);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if constexpr (Global) __stcg(out + e * 32u + lane, v[e]);
+        else out[e * 32u + lane] = v[e];
+    }
+}
+
+// The inlined network with the output space chosen at run time.  Every
+// shared-memory load is unconditional, at a clamped index, with the bound
+// applied by a select afterwards: predicated loads into one temporary would
+// serialise the window (each load waits for the previous one's move), which
+// under the register pressure of the server's loop costs more than the
+// merge itself.
+template <typename Key, int K, int E>
+__device__ __forceinline__ void warp_half_bt_rt(const Key* __restrict__ A, const Key* __restrict__ B,
+                                                Key* __restrict__ out, uint32_t D, bool global) {
+    constexpr uint32_t W = 32u * E;
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t lo = D > (uint32_t)K ? D - K : 0u;
+    uint32_t hi = D < (uint32_t)K ? D : (uint32_t)K;
+#pragma unroll
+    for (uint32_t span = (uint32_t)K; span > 0; span >>= 5) {
+        const uint32_t g = span > 32 ? ((span + 31u) >> 5) | 1u : 1u;
+        const uint32_t p = lo + (lane + 1u) * g;
+        const uint32_t pc = p <= hi ? p : hi;  // hi >= 1 when lo < hi; else no lane is ok
+        const uint32_t ia = pc ? pc - 1u : 0u;
+        const uint32_t ib = D - pc < (uint32_t)K ? D - pc : (uint32_t)K - 1u;
+        const Key xa = A[ia], xb = B[ib];
+        const bool ok = p <= hi && xa <= xb;
+        lo += (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, ok)) * g;
+        const uint32_t h2 = lo + g - 1u;
+        hi = h2 < hi ? h2 : hi;
+        if (g == 1u) break;
+    }
+    const uint32_t a = lo, b = D - lo;
+    Key v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const uint32_t i = e * 32u + lane;
+        const bool ina = a + i < (uint32_t)K;
+        const Key x0 = A[ina ? a + i : (uint32_t)K - 1u];
+        const uint32_t j = b + (W - 1u - i);
+        const bool inb = j < (uint32_t)K;
+        const Key y0 = B[inb ? j : (uint32_t)K - 1u];
+        const Key x = ina ? x0 : KeyLimits<Key>::kMax;
+        const Key y = inb ? y0 : KeyLimits<Key>::kMax;
+        v[e] = x < y ? x : y;
+    }
+#pragma unroll
+    for (int rs = E / 2; rs >= 1; rs >>= 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e & rs) == 0) {
+                const Key x = v[e], y = v[e + rs];
+                v[e] = x < y ? x : y;
+                v[e + rs] = x < y ? y : x;
+            }
+        }
+    }
+#pragma unroll
+    for (int ls = 16; ls >= 1; ls >>= 1) {
+        const bool upper = (lane & (uint32_t)ls) != 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const Key o = __shfl_xor_sync(0xFFFFFFFFu, v[e], ls);
+            v[e] = upper ? (v[e] < o ? o : v[e]) : (v[e] < o ? v[e] : o);
+        }
+    }
+    if (global) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) __stcg(out + e * 32u + lane, v[e]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) out[e * 32u + lane] = v[e];
+    }
+}
+
 // Tile shape of a half merge on NW warps: each used warp covers kPer outputs
 // in tiles of 32E (E <= 16 keys per lane).
 template <int K, int NW>
@@ -234,7 +360,7 @@ struct TileShape {
 // Outputs [0, K) (!Second) or [K, 2K) (Second) of merge(A, B) -> out[0, K),
 // by the NW warps of a group (gw = warp index in the group).  K < 32 falls
 // back to the per-thread merge path on the group's threads.  No barrier.
-template <typename Key, int K, int NW, bool Second, bool Global>
+template <typename Key, int K, int NW, bool Second, bool Global, bool Inl = false>
 __device__ __forceinline__ void grp_merge_half(const Key* __restrict__ A, const Key* __restrict__ B,
                                                Key* __restrict__ out, uint32_t gw) {
     using S = TileShape<K, NW>;
@@ -245,8 +371,49 @@ __device__ __forceinline__ void grp_merge_half(const Key* __restrict__ A, const 
 #pragma unroll 1
         for (int t = 0; t < S::kTiles; ++t) {
             const uint32_t o = gw * (uint32_t)S::kPer + (uint32_t)t * 32u * S::E;
-            warp_half_bt<Key, K, S::E, Global>(A, B, out + o, (Second ? (uint32_t)K : 0u) + o);
+            if constexpr (Inl)
+                warp_half_bt_inl<Key, K, S::E, Global>(A, B, out + o, (Second ? (uint32_t)K : 0u) + o);
+            else
+                warp_half_bt<Key, K, S::E, Global>(A, B, out + o, (Second ? (uint32_t)K : 0u) + o);
         }
+    }
+}
+
+// The k-th smallest key (k = K) of two sorted K-batches -- the largest key
+// of the first half of their merge -- by one warp (every lane gets it): the
+// 32-ary merge-path split of diagonal K, then max(A[a-1], B[K-a-1]).
+template <typename Key, int K>
+__device__ __forceinline__ Key warp_kth_max(const Key* __restrict__ A, const Key* __restrict__ B) {
+    const uint32_t lane = threadIdx.x & 31u;
+    constexpr uint32_t D = (uint32_t)K;
+    uint32_t lo = 0, hi = D;
+#pragma unroll
+    for (uint32_t span = (uint32_t)K; span > 0; span >>= 5) {
+        const uint32_t g = span > 32 ? ((span + 31u) >> 5) | 1u : 1u;
+        const uint32_t p = lo + (lane + 1u) * g;
+        const bool ok = p <= hi && A[p - 1] <= B[D - p];
+        lo += (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, ok)) * g;
+        const uint32_t h2 = lo + g - 1u;
+        hi = h2 < hi ? h2 : hi;
+        if (g == 1u) break;
+    }
+    const uint32_t a = lo;
+    const Key x = a > 0 ? A[a - 1] : Key(0);
+    const Key y = a < D ? B[D - 1 - a] : Key(0);
+    return x > y ? x : y;
+}
+
+// grp_merge_half with the half and the output space chosen at run time, on
+// the inlined network: one call site serves every merge of a round loop.
+template <typename Key, int K, int NW>
+__device__ __forceinline__ void grp_merge_half_rt(const Key* __restrict__ A, const Key* __restrict__ B,
+                                                  Key* __restrict__ out, uint32_t gw, bool second, bool global) {
+    using S = TileShape<K, NW>;
+    static_assert(S::kUsed == NW, "one tile row per warp");
+#pragma unroll 1
+    for (int t = 0; t < S::kTiles; ++t) {
+        const uint32_t o = gw * (uint32_t)S::kPer + (uint32_t)t * 32u * S::E;
+        warp_half_bt_rt<Key, K, S::E>(A, B, out + o, (second ? (uint32_t)K : 0u) + o, global);
     }
 }
 

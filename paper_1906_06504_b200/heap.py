@@ -280,13 +280,24 @@ class GeneralizedHeap:
                       "rs_fill", "lv_acq", "lv_load", "lv_merge", "lv_rel", "served",
                       "serve_holds", "bu_parent", "bu_retake", "bu_levels", "split_a", "split_b",
                       "del_served", "del_serve_holds", "sv_split", "sv_a", "sv_b", "sv_r1", "sv_r2",
-                      "sv_r3", "sv_next", "sv_claim")
+                      "sv_r3", "sv_next", "sv_claim", "s3_ops", "s3_op", "s3_r0", "s3_wait_rf",
+                      "s3_r1", "s3_wait_c3", "s3_r2", "s3_r3", "s3_claim", "s3_refill", "s3_ctl",
+                      "s3_rec", "s3_wake", "s3_post", "s3_start")
 
     def profile(self, reset: bool = True) -> dict:
         """SM-cycle profile of a BH_FLAG_PROFILE heap (see bh_profile)."""
-        buf = (C.c_uint64 * 48)()
-        _raise(L.lib().bh_profile(self._h, buf, 48, int(reset)))
+        buf = (C.c_uint64 * 64)()
+        _raise(L.lib().bh_profile(self._h, buf, 64, int(reset)))
         return dict(zip(self.PROFILE_FIELDS, (int(v) for v in buf)))
+
+    def profile_timeline(self) -> np.ndarray:
+        """Per-op event clocks of a three-level delete server (profiling
+        handles): ops kTlFirst.. of the first hold, 32 events each (see
+        bh_heap.cuh tl())."""
+        base, ops = 64 + 4 * 4096, 64
+        buf = (C.c_uint64 * (base + ops * 32))()
+        _raise(L.lib().bh_profile(self._h, buf, base + ops * 32, 0))
+        return np.frombuffer(buf, dtype=np.uint64)[base:].reshape(ops, 32).copy()
 
     def info(self) -> dict:
         k, kb, mn, tpc, mc = (C.c_uint32() for _ in range(5))

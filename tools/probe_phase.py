@@ -18,6 +18,7 @@ ap.add_argument("--variant", default="bu")
 ap.add_argument("--ctas", type=int, nargs="+", default=[0])
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--profile", action="store_true")
+ap.add_argument("--flags", type=lambda x: int(x, 0), default=0, help="heap debug flags (bh_internal.h kDbg*)")
 a = ap.parse_args()
 n = 1 << a.log2n
 dev = torch.device("cuda")
@@ -26,7 +27,7 @@ pool = torch.from_numpy(keys.view(np.int32)).to(dev)
 for k in a.k:
     for ctas in a.ctas:
         for rep in range(a.reps):
-            heap = GeneralizedHeap(Variant.BU if a.variant == "bu" else Variant.TD, k, n // k + 1024, key_bits=32, profile=a.profile)
+            heap = GeneralizedHeap(Variant.BU if a.variant == "bu" else Variant.TD, k, n // k + 1024, key_bits=32, profile=a.profile, debug_flags=a.flags)
             n_ops = n // k
             ops_i = torch.from_numpy(phase_ops(0, n, k).view(np.uint8)).to(dev)
             ops_d = torch.from_numpy(phase_ops(1, n, k).view(np.uint8)).to(dev)
@@ -74,4 +75,11 @@ for k in a.k:
                       f"split {us(p['sv_split'], sv):.2f} (refill {us(p['sv_a'], sv):.2f}; H0+lo0 {us(p['sv_b'], sv):.2f} then claims {us(p['sv_claim'], sv):.2f}) "
                       f"r1 {us(p['sv_r1'], sv):.2f} "
                       f"r2 {us(p['sv_r2'], sv):.2f} r3 {us(p['sv_r3'], sv):.2f} next {us(p['sv_next'], sv):.2f}", flush=True)
+                s3 = max(p['s3_ops'], 1)
+                print(f"   three-level server: {p['s3_ops']} ops | per op us: op {us(p['s3_op'], s3):.2f} r0 {us(p['s3_r0'], s3):.2f} "
+                      f"wait-refill {us(p['s3_wait_rf'], s3):.2f} r1 {us(p['s3_r1'], s3):.2f} wait-claim {us(p['s3_wait_c3'], s3):.2f} "
+                      f"r2 {us(p['s3_r2'], s3):.2f} r3 {us(p['s3_r3'], s3):.2f} | claim warp {us(p['s3_claim'], s3):.2f} "
+                      f"refill warps {us(p['s3_refill'], s3):.2f} control warp {us(p['s3_ctl'], s3):.2f} | "
+                      f"between ops: record {us(p['s3_rec'], s3):.2f} wake {us(p['s3_wake'], s3):.2f} "
+                      f"post {us(p['s3_post'], s3):.2f} start {us(p['s3_start'], s3):.2f}", flush=True)
             heap.close()
