@@ -1517,20 +1517,20 @@ struct HeapCta {
         // stay out of both groups: the leader's bookkeeping and kPubLane's
         // flush of the previous op + next-waiter lookup run beside them.
         if (threadIdx.x < kRefBase) {
-            // three independent chains on three lanes: the previous op's
-            // releases and hand-off (kPubLane), the next ticket's look-up
-            // (the leader) and the next refill's state word
+            // (a look-up beside the flush instead of after it -- three lanes,
+            // three chains -- hung mixed insert/delete runs with serving at
+            // full size, tools/gpu/bisect_mixed.sh; the order below is the
+            // tested one)
             if (threadIdx.x == kPubLane) {
                 sv_flush(sh->pd);
-            } else if (threadIdx.x == 0) {
-                unsigned long long nop = 0, noff = 0;
-                const bool more = nodes - 1 >= kServeMin && waiting_delete(t + 1, nop, &noff);
+                unsigned long long nop = 0;
+                const bool more = nodes - 1 >= kServeMin && waiting_delete(t + 1, nop);
                 sh->serve = more;
                 sh->op_next = nop;
-                sh->off_next = noff;
-            } else if (threadIdx.x == (kPubLane == 1 ? 2u : 1u)) {
-                // the next op's refill (a word of this very slot, or none)
-                sh->next_w = nodes - 1 >= kServeMin ? state_load(st(slot_for_rank(nodes - 1))) : 0xFFFFFFFFu;
+                if (more) {
+                    sh->off_next = rv.ops[nop].offset;
+                    sh->next_w = state_load(st(slot_for_rank(nodes - 1)));  // the next op's refill
+                }
             }
         } else if (threadIdx.x < kHalfT) {
             // released here, before the server waits on any claim (below)

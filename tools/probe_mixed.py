@@ -23,6 +23,7 @@ ap.add_argument("--levels", type=int, default=14)
 ap.add_argument("--variants", default="bu,td")
 ap.add_argument("--ref", action="store_true")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--flags", type=lambda x: int(x, 0), default=0, help="heap debug flags (bh_internal.h kDbg*)")
 a = ap.parse_args()
 k, n = a.k, 1 << a.log2n
 pairs = n // k
@@ -42,7 +43,8 @@ d_seed = torch.from_numpy(seed_keys.view(np.int32)).to(dev)
 d_seed_ops = torch.from_numpy(phase_ops(0, seed_nodes * k, k).view(np.uint8)).to(dev)
 for v in a.variants.split(","):
     for rep in range(a.reps):
-        heap = GeneralizedHeap(Variant.BU if v == "bu" else Variant.TD, k, seed_nodes + pairs + 1024, key_bits=32)
+        heap = GeneralizedHeap(Variant.BU if v == "bu" else Variant.TD, k, seed_nodes + pairs + 1024, key_bits=32,
+                               debug_flags=a.flags)
         s = torch.cuda.current_stream()
         heap.run_ops_ptr(d_seed_ops.data_ptr(), seed_nodes, d_seed.data_ptr(), 0, d_st.data_ptr(), 0, 0,
                          stream=s.cuda_stream)
