@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--ctas", type=int, default=0, help="persistent CTAs (0 = all co-resident)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the u64 line and the profiled root-service run (outside the timed region)")
     return ap.parse_args()
 
 
@@ -89,6 +91,10 @@ def ncu_traffic(k: int, log2n: int, variant: str):
         return d.get(f"{variant}_k{k}_n{log2n}_delete")
     except Exception:
         return None
+
+
+def stats(xs):
+    return {"min": min(xs), "median": statistics.median(xs), "max": max(xs), "n": len(xs)}
 
 
 # ------------------------------------------------------------- clocks ----
@@ -197,6 +203,91 @@ def run_reference_arm(a, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------- extras ----
+def root_service(a, dev, keys, stream, flush, value):
+    """The root-serial bound: every op holds the root (or
+    its delete server's turn) for t_root, so no schedule beats
+    N / ((N/K) * (t_root_ins + t_root_del)) round-trip keys/s, i.e. twice
+    that in key-ops/s.  t_root from one BH_FLAG_PROFILE step outside the
+    timed region (profiling adds its own cycles: an upper estimate of
+    t_root, so the fraction below is a lower estimate)."""
+    import numpy as np
+    import torch
+    from paper_1906_06504_b200 import GeneralizedHeap, Variant, phase_ops
+    k, n = a.k, 1 << a.log2n
+    n_ops = (n + k - 1) // k
+    heap = GeneralizedHeap(Variant.BU if a.variant == "bu" else Variant.TD, k, n_ops + 1024, key_bits=32,
+                           profile=True, device=dev.index or 0)
+    pool = torch.from_numpy(keys.view(np.int32)).to(dev)
+    ops_i = torch.from_numpy(phase_ops(0, n, k).view(np.uint8)).to(dev)
+    ops_d = torch.from_numpy(phase_ops(1, n, k).view(np.uint8)).to(dev)
+    out = torch.empty(n_ops * k, dtype=torch.int32, device=dev)
+    with torch.cuda.stream(stream):
+        flush.fill_(4)
+    stream.synchronize()
+    heap.run_ops_ptr(ops_i.data_ptr(), n_ops, pool.data_ptr(), 0, 0, 0, 0, ctas=a.ctas, stream=stream.cuda_stream)
+    stream.synchronize()
+    p_ins = heap.profile(reset=True)
+    heap.run_ops_ptr(ops_d.data_ptr(), n_ops, 0, out.data_ptr(), 0, 0, 0, ctas=a.ctas, stream=stream.cuda_stream)
+    stream.synchronize()
+    p = heap.profile(reset=True)
+    heap.close()
+    ghz = 1.965  # B200 SM clock under load (the clocks sampled above)
+    us = lambda c, m: c / max(m, 1) / (ghz * 1e3)
+    t_ins = us(p_ins["ins_root_hold"], p_ins["ins_ops"])
+    served = p["del_served"] + p["del_serve_holds"]
+    sv = sum(p[f] for f in ("sv_split", "sv_r1", "sv_r2", "sv_r3", "sv_next"))
+    t_del_served = us(sv, served)
+    t_del_plain = us(p["del_root_hold"], p["del_ops"] - served)
+    t_del = (served * t_del_served + (p["del_ops"] - served) * t_del_plain) / max(p["del_ops"], 1)
+    bound = 2 * n / (n_ops * (t_ins + t_del) * 1e-6)
+    return {"t_root_insert_us": t_ins, "t_root_delete_us": t_del,
+            "deletes_served": served, "delete_ops": p["del_ops"],
+            "bound_key_ops_per_s": bound, "achieved_frac_of_bound": value / bound,
+            "source": "one BH_FLAG_PROFILE step outside the timed region: mean root hold per insert "
+                      "(combining holds included) + per-op delete-server service time"}
+
+
+def u64_line(a, dev, world):
+    """The same step at the reference's own key width (u64, batch.hpp:17)."""
+    import numpy as np
+    import torch
+    from paper_1906_06504_b200 import GeneralizedHeap, Variant, generate_keys, phase_ops
+    k, n = a.k, 1 << a.log2n
+    n_ops = (n + k - 1) // k
+    keys = generate_keys(n, 1, key_bits=64)
+    pool = torch.from_numpy(keys.view(np.int64)).to(dev)
+    ops_i = torch.from_numpy(phase_ops(0, n, k).view(np.uint8)).to(dev)
+    ops_d = torch.from_numpy(phase_ops(1, n, k).view(np.uint8)).to(dev)
+    out = torch.empty(n_ops * k, dtype=torch.int64, device=dev)
+    seq = torch.empty(n_ops, dtype=torch.int64, device=dev)
+    heap = GeneralizedHeap(Variant.BU if a.variant == "bu" else Variant.TD, k, n_ops + 1024, key_bits=64,
+                           device=dev.index or 0)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    times = []
+    for i in range(2 + max(2, a.steps // 2)):
+        with torch.cuda.stream(stream):
+            flush.fill_(5)
+        stream.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        heap.run_ops_ptr(ops_i.data_ptr(), n_ops, pool.data_ptr(), 0, 0, 0, 0, ctas=a.ctas, stream=stream.cuda_stream)
+        heap.run_ops_ptr(ops_d.data_ptr(), n_ops, 0, out.data_ptr(), 0, 0, seq.data_ptr(), ctas=a.ctas,
+                         stream=stream.cuda_stream)
+        ev[1].record(stream)
+        stream.synchronize()
+        if i >= 2:
+            times.append(ev[0].elapsed_time(ev[1]))
+    drained = out.view(n_ops, k)[torch.argsort(seq)].reshape(-1)[:n]
+    ok = bool(torch.equal(drained, torch.sort(pool).values))  # keys < 2^63: signed order == unsigned
+    heap.close()
+    ms = statistics.mean(times)
+    return {"value": world * 2 * n / (ms / 1e3), "unit": UNIT, "dtype": "u64", "ms_per_step": ms,
+            "ms_per_step_stats": stats(times), "checked_sorted": ok,
+            "workload": f"as config, generate_keys(2^{a.log2n}, seed 1) as uint64 keys"}
+
+
 # ------------------------------------------------------------------ ours --
 def run_ours(a, rank: int, world: int, dist):
     import numpy as np
@@ -269,7 +360,6 @@ def run_ours(a, rank: int, world: int, dist):
         t_ins.append(ti)
         t_del.append(td)
         t_step.append(ti + td)
-    clocks = sampler.stop() if sampler else None
 
     ms = statistics.mean(t_step)
     if dist:
@@ -304,11 +394,21 @@ def run_ours(a, rank: int, world: int, dist):
             t = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
+        # the e2e result is checked too: the last drain, in sequence order,
+        # is the sorted input
+        e_out = h_out.to(dev).view(n_ops, k)[torch.argsort(h_seq.to(dev))].reshape(-1)[:n]
+        if not torch.equal(e_out.to(torch.int64) & 0xFFFFFFFF, ref_sorted):
+            raise SystemExit("bench: e2e drain != sorted(input) -- refusing to report")
         h2d = n * 4 + 2 * n_ops * 16
         d2h = n_ops * k * 4 + n_ops * 8
         e2e = {"value": world * 2 * n / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": te * 1e3,
-               "path": "bh_run_ops (C ABI) x2, pinned host buffers, copies + kernels + sync"}
+               "ms_per_step_stats": stats([x * 1e3 for x in e2e_times]),
+               "value_stats": stats([world * 2 * n / x for x in e2e_times]),
+               "path": "bh_run_ops (C ABI) x2, pinned host buffers, copies + kernels + sync",
+               "checked": "last drain == sorted(input)"}
+    # clocks sampled over both arms (device-timed steps and e2e steps)
+    clocks = sampler.stop() if sampler else None
 
     if rank != 0:
         return
@@ -317,6 +417,7 @@ def run_ours(a, rank: int, world: int, dist):
     td_mean = statistics.mean(t_del) / 1e3
     ti_mean = statistics.mean(t_ins) / 1e3
     achieved = del_b / td_mean / 1e9
+    step_s = ms / 1e3
     roofline = {"bound": "hbm", "kernel": "heap_ops_kernel (deleteMin phase launch)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(k, a.log2n, a.variant),
@@ -324,6 +425,8 @@ def run_ours(a, rank: int, world: int, dist):
                 "algorithmic_bytes_per_launch": del_b,
                 "insert_launch": {"achieved": ins_b / ti_mean / 1e9, "algorithmic_bytes": ins_b,
                                   "frac": ins_b / ti_mean / 1e9 / peak},
+                "whole_step": {"achieved": (ins_b + del_b) / step_s / 1e9, "algorithmic_bytes": ins_b + del_b,
+                               "frac": (ins_b + del_b) / step_s / 1e9 / peak},
                 "walk_model": "SURVEY.md 8(d): whole-node read/write per level, no early-stop credit"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
@@ -336,12 +439,23 @@ def run_ours(a, rank: int, world: int, dist):
                    "ctas": a.ctas or heap.max_ctas, "l2": "256 MB buffer written between timed steps",
                    "parallelism": f"replicas x{world}"},
         "insert_ms": statistics.mean(t_ins), "delete_ms": statistics.mean(t_del),
+        "ms_per_step_stats": stats(t_step), "insert_ms_stats": stats(t_ins), "delete_ms_stats": stats(t_del),
+        "value_stats": stats([world * 2 * n / (x / 1e3) for x in t_step]),
         "rt_keys_per_s": world * n / (ms / 1e3),
         "roofline": roofline, "clocks": clocks, "gpu_launches": 2 * a.steps,
         "correctness": "drain == sorted(input) checked on device before timing",
     }
     if e2e:
         line["e2e"] = e2e
+    if not a.no_extras:
+        heap.close()
+        del out, seq, pool
+        torch.cuda.empty_cache()
+        line["root_serial_bound"] = root_service(a, dev, keys, stream, flush, value)
+        line["u64"] = u64_line(a, dev, world)
+    ref_matrix = os.path.join(ROOT, "profiles", "r2", "ref_matrix.json")
+    if os.path.exists(ref_matrix):
+        line["cpu_baseline_matrix"] = os.path.relpath(ref_matrix, ROOT)
     if not a.no_cpu_baseline and world == 1:
         try:
             threads = host_threads()

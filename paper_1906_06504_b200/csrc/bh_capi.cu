@@ -11,6 +11,9 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <cstdlib>
+#include <thread>
+#include <chrono>
 #include <random>
 #include <string>
 #include <vector>
@@ -253,6 +256,52 @@ void put_ctx(bh_heap* h, OpCtx* c) {
 // Device-detected protocol faults (reference: the std::logic_error
 // "sentinel escaped" of heap.cpp:462-463 and asserts) after a synchronous
 // call: BH_E_INTERNAL with the flags named.
+// Host side of the deadlock watchdog (the reference's watchdog thread,
+// proj/src/workload.cpp:22-53): a synchronous run waits for its stream with
+// a deadline (BH_RUN_TIMEOUT_S, default 600 s, 0 = none) instead of blocking
+// in cudaStreamSynchronize forever.  On expiry it reads the header's error
+// flags on the non-blocking aux stream (a wait that spun past ~4 s set
+// kErrStuck, bh_device.cuh Backoff) and returns BH_E_INTERNAL; the kernel
+// itself cannot be cancelled, so the caller should tear the process down.
+double run_timeout_s() {
+    const char* e = std::getenv("BH_RUN_TIMEOUT_S");
+    if (!e || !*e) return 600.0;
+    return std::atof(e);
+}
+
+int wait_with_watchdog(bh_heap* h, cudaStream_t s) {
+    const double limit = run_timeout_s();
+    if (limit <= 0) {
+        const cudaError_t e0 = cudaStreamSynchronize(s);
+        return e0 == cudaSuccess ? BH_OK : cuda_fail(e0, "run");
+    }
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "watchdog event");
+    if ((e = cudaEventRecord(ev, s)) != cudaSuccess) {
+        cudaEventDestroy(ev);
+        return cuda_fail(e, "watchdog event");
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t spin = 0;; ++spin) {
+        e = cudaEventQuery(ev);
+        if (e != cudaErrorNotReady) break;
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (dt > limit) {
+            cudaEventDestroy(ev);
+            unsigned long long flags = 0;
+            cudaMemcpyAsync(&flags, reinterpret_cast<const char*>(h->d_hdr) + offsetof(Header, error_flags),
+                            sizeof(flags), cudaMemcpyDeviceToHost, h->aux);
+            cudaStreamSynchronize(h->aux);
+            return fail(BH_E_INTERNAL, "deadlock watchdog: run not finished after " + std::to_string(limit) +
+                                           " s" + ((flags & kErrStuck) ? " (a device wait spun past ~4 s)" : ""));
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(spin > 1024 ? 200 : 20));
+    }
+    cudaEventDestroy(ev);
+    return e == cudaSuccess ? BH_OK : cuda_fail(e, "run");
+}
+
 int check_device_faults(bh_heap* h) {
     unsigned long long flags = 0;
     cudaError_t e = cudaMemcpy(&flags, reinterpret_cast<const char*>(h->d_hdr) + offsetof(Header, error_flags),
@@ -264,6 +313,7 @@ int check_device_faults(bh_heap* h) {
     if (flags & kErrInteriorEmpty) msg += " interior node empty;";
     if (flags & kErrEventOverflow) msg += " event log overflow;";
     if (flags & kErrRetake) msg += " parked slot taken during a gated climb;";
+    if (flags & kErrStuck) msg += " a device wait spun past ~4 s;";
     return fail(BH_E_INTERNAL, msg);
 }
 
@@ -302,7 +352,13 @@ int single_op(bh_heap* h, const bh_op& op, const void* keys, uint32_t n, void* o
     const size_t down_end = out ? lay.out + (size_t)h->k * h->key_size : lay.keys;
     e = cudaMemcpyAsync(c->h + lay.status, c->d + lay.status, down_end - lay.status,
                         cudaMemcpyDeviceToHost, c->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) {
+        const int w = wait_with_watchdog(h, c->stream);
+        if (w != BH_OK) {
+            put_ctx(h, c);
+            return w;
+        }
+    }
     if (e != cudaSuccess) {
         put_ctx(h, c);
         return cuda_fail(e, "single_op run");
@@ -566,6 +622,10 @@ int bh_run_ops(bh_heap* h, const bh_op* ops, uint64_t n_ops, const void* key_poo
     c2.flags |= BH_RUN_EXPLICIT_STREAM;
     int rc = bh_run_ops_device(h, d_ops, n_ops, d_pool, d_out, d_status, d_lens, d_seq, &c2);
     if (rc != BH_OK) return rc;
+    // the watchdog's wait comes before the copies back: a copy into pageable
+    // memory would block on the kernel itself
+    const int w = wait_with_watchdog(h, s);
+    if (w != BH_OK) return w;
     if (out_pool && out_pool_len)
         BH_CUDA(cudaMemcpyAsync(out_pool, d_out, out_pool_len * h->key_size, cudaMemcpyDeviceToHost, s));
     if (out_status) BH_CUDA(cudaMemcpyAsync(out_status, d_status, n_ops * 4, cudaMemcpyDeviceToHost, s));

@@ -212,20 +212,34 @@ __device__ __forceinline__ void grp_fill_max(Key* g, uint32_t n, uint32_t tid, u
 // lock holder's SM and the contended L2 slice stay free.
 // The first polls spin without sleeping: a lock hand-off on the critical
 // path should cost one L2 round trip, not a sleep quantum.
+// Device side of the deadlock watchdog (the reference's is a host thread,
+// proj/src/workload.cpp:22-53): a wait that passes kStuckSpins pauses (about
+// 4 s of 256 ns sleeps) raises a flag word (the heap header's error flags)
+// once; the host watchdog of bh_run_ops reports it.
+constexpr uint32_t kStuckSpins = 1u << 24;
+constexpr unsigned long long kStuckFlag = 1ull << 4;  // = kErrStuck (bh_internal.h)
 struct Backoff {
     uint32_t n = 0;
+    unsigned long long* stuck = nullptr;
+    __device__ __forceinline__ Backoff() {}
+    __device__ __forceinline__ explicit Backoff(unsigned long long* flag_word) : stuck(flag_word) {}
     __device__ __forceinline__ void pause() {
         ++n;
         if (n > 32) __nanosleep(n > 64 ? 256 : 64);
+        if (n == kStuckSpins && stuck) atomicOr(stuck, kStuckFlag);
     }
 };
 // For a waiter whose wake-up is on a critical path (a delete that a delete
 // server may hand a continuation): short sleeps only.
 struct QuickBackoff {
     uint32_t n = 0;
+    unsigned long long* stuck = nullptr;
+    __device__ __forceinline__ QuickBackoff() {}
+    __device__ __forceinline__ explicit QuickBackoff(unsigned long long* flag_word) : stuck(flag_word) {}
     __device__ __forceinline__ void pause() {
         ++n;
         if (n > 32) __nanosleep(32);
+        if (n == (kStuckSpins << 3) && stuck) atomicOr(stuck, kStuckFlag);
     }
 };
 
@@ -309,10 +323,11 @@ __device__ __forceinline__ void cta_fill(Key* g, Key v, uint32_t n) {
 }
 
 // ------------------------------------------------------------- sorting --
-// Block bitonic sort of K keys in shared memory (section 4.1).  The
-// stages whose compare distance stays inside one thread's register pair are
-// done in registers; the wider ones go through shared memory.  Ends with a
-// barrier.  Caller pads unused tail slots with the sentinel.
+// Block bitonic sort of K keys in shared memory (section 4.1), every
+// stage through shared memory with a CTA barrier.  Kept for node capacities
+// below 32 (fewer keys than threads); cta_sort_batch below is the batch sort
+// of every larger node.  Ends with a barrier.  Caller pads unused tail slots
+// with the sentinel.
 template <typename Key, int K, int T>
 __device__ __forceinline__ void cta_bitonic_sort(Key* s) {
     if constexpr (K >= 2) {
@@ -338,6 +353,101 @@ __device__ __forceinline__ void cta_bitonic_sort(Key* s) {
     } else {
         __syncthreads();
     }
+}
+
+// sort_batch (proj/src/batch.cpp:7-19) of one incoming batch: n <= K keys at
+// g (global), sentinel-padded to K, sorted ascending into s0 (shared).  A
+// register bitonic network: thread t holds keys [tE, tE + E), E = K / T,
+// loaded as one E-key vector when aligned (8 or 16 bytes); compare-exchange
+// stages of stride < E stay in the thread's registers, strides E..16E go
+// through warp shuffles, and only strides >= 32E pass through shared memory,
+// ping-ponging between s0 and s1 with one barrier per stage (10 of the 55
+// stages at K = 1024, T = 512).  Returns, uniformly over the CTA, whether a
+// key reached the sentinel (batch.cpp:13-15).  Ends with a barrier.
+template <typename Key, int K, int T>
+__device__ __forceinline__ bool cta_sort_batch(const Key* __restrict__ g, uint32_t n, Key* s0, Key* s1) {
+    constexpr int E = K / T;
+    static_assert(E >= 1 && E * T == K, "K must be a multiple of the CTA size");
+    constexpr Key kMax = KeyLimits<Key>::kMax;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t base = threadIdx.x * E;
+    Key v[E];
+    constexpr uint32_t kVecBytes = E * sizeof(Key);
+    const bool whole = base + E <= n;
+    if constexpr (kVecBytes == 16 || kVecBytes == 8) {
+        if (whole && ((uintptr_t)(g + base) % kVecBytes) == 0) {
+            if constexpr (kVecBytes == 16) {
+                const uint4 x = *reinterpret_cast<const uint4*>(g + base);
+                const Key* px = reinterpret_cast<const Key*>(&x);
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = px[e];
+            } else {
+                const uint2 x = *reinterpret_cast<const uint2*>(g + base);
+                const Key* px = reinterpret_cast<const Key*>(&x);
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = px[e];
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = base + e < n ? g[base + e] : kMax;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = base + e < n ? g[base + e] : kMax;
+    }
+    int bad = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) bad |= (base + e < n) && v[e] >= kMax;
+    bad = __syncthreads_or(bad);
+    if (bad) return true;
+    uint32_t par = 0;
+#pragma unroll
+    for (uint32_t size = 2; size <= (uint32_t)K; size <<= 1) {
+#pragma unroll
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32u * E) {  // partner in another warp
+                Key* sb = par ? s1 : s0;
+                par ^= 1u;
+#pragma unroll
+                for (int e = 0; e < E; ++e) sb[base + e] = v[e];
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const uint32_t i = base + e;
+                    const Key o = sb[i ^ stride];
+                    const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
+                    v[e] = keep_min ? (o < v[e] ? o : v[e]) : (o < v[e] ? v[e] : o);
+                }
+            } else if (stride >= (uint32_t)E) {  // partner in another lane of the warp
+                const int d = (int)(stride / E);
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const uint32_t i = base + e;
+                    const Key o = __shfl_xor_sync(0xFFFFFFFFu, v[e], d);
+                    const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
+                    v[e] = keep_min ? (o < v[e] ? o : v[e]) : (o < v[e] ? v[e] : o);
+                }
+            } else {  // partner in this thread's registers
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if ((e & (int)stride) == 0) {
+                        const int f = e + (int)stride;
+                        const bool up = ((base + e) & size) == 0;
+                        const Key x = v[e], y = v[f];
+                        const bool sw = up ? (y < x) : (x < y);
+                        v[e] = sw ? y : x;
+                        v[f] = sw ? x : y;
+                    }
+                }
+            }
+        }
+    }
+    (void)lane;
+    __syncthreads();  // the last shared-memory stage's reads are done
+#pragma unroll
+    for (int e = 0; e < E; ++e) s0[base + e] = v[e];
+    __syncthreads();
+    return false;
 }
 
 // ------------------------------------------------------------- merging --

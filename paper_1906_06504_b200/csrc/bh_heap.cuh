@@ -48,6 +48,8 @@
 
 namespace bh {
 
+static_assert(kStuckFlag == kErrStuck, "watchdog flag bit");
+
 // Releases a delete server has deferred to its next op (kPubLane only).
 struct SvPending {
     unsigned long long slot[5];
@@ -373,7 +375,7 @@ struct HeapCta {
         if (del_req) {
             // words 0-1 in one load: a delete server's hand-off puts the
             // continuation word (serve_deletes) next to the flag
-            QuickBackoff b;
+            QuickBackoff b(&hdr->error_flags);
             unsigned long long vv;
             while ((((uint32_t)(vv = ld_acquire_u64(reinterpret_cast<const unsigned long long*>(f)))) & ~1u) !=
                    granted) {
@@ -383,7 +385,7 @@ struct HeapCta {
             v = (uint32_t)vv;
             sh->contw = (uint32_t)(vv >> 32);
         } else {
-            Backoff b;
+            Backoff b(&hdr->error_flags);
             while (((v = state_load(f)) & ~1u) != granted) { b.pause(); BH_WAIT_NOTE(__LINE__); }
         }
         sh->root_tk = t;
@@ -455,7 +457,7 @@ struct HeapCta {
     // INUSE.  Returns the state it was claimed from.  Calling lane only.
     __device__ uint32_t lane_claim(unsigned long long slot, uint32_t accept, uint32_t* claimed_word = nullptr) {
         uint32_t* p = st(slot);
-        Backoff b;
+        Backoff b(&hdr->error_flags);
         for (;;) {
             const uint32_t w = state_load(p);
             if (((accept >> sget(w)) & 1u) && state_cas(p, w, swith(w, kInUse))) {
@@ -527,7 +529,7 @@ struct HeapCta {
     // close the running phase.
     __device__ void gate_wait(bool climb) {
         const unsigned long long me = climb ? 0ull : 1ull;
-        Backoff b;
+        Backoff b(&hdr->error_flags);
         for (;;) {
             const unsigned long long ph = __ldcg(&hdr->gate_phase);
             const unsigned long long closing = __ldcg(&hdr->gate_closing);
@@ -593,20 +595,26 @@ struct HeapCta {
         const unsigned long long t0 = now();
         Key* sorted = buf(0);
         const Key* src = static_cast<const Key*>(rv.key_pool) + o.offset;
-        int bad = 0;
-        for (uint32_t i = threadIdx.x; i < (uint32_t)K; i += T) {
-            Key v = kMaxKey;
-            if (i < n) {
-                v = src[i];
-                bad |= v >= kMaxKey;
+        bool bad;
+        if constexpr (K >= T) {
+            bad = cta_sort_batch<Key, K, T>(src, n, sorted, buf(1));  // buf(1) is free until the root phase
+        } else {
+            int b = 0;
+            for (uint32_t i = threadIdx.x; i < (uint32_t)K; i += T) {
+                Key v = kMaxKey;
+                if (i < n) {
+                    v = src[i];
+                    b |= v >= kMaxKey;
+                }
+                sorted[i] = v;
             }
-            sorted[i] = v;
+            bad = __syncthreads_or(b) != 0;
+            if (!bad) cta_bitonic_sort<Key, K, T>(sorted);
         }
-        if (__syncthreads_or(bad)) {  // batch.cpp:13-15, before any mutation
+        if (bad) {  // batch.cpp:13-15, before any mutation
             status(opi, BH_E_INVALID_KEY, 0, ~0ull);
             return;
         }
-        cta_bitonic_sort<Key, K, T>(sorted);
         rec(kEvInv, 0);
         const unsigned long long t1 = now();
 
@@ -769,7 +777,7 @@ struct HeapCta {
         Key* tmp = buf(5);
         if (leader()) {  // claim the target under the root lock: AVAIL -> TARGET
             uint32_t* p = st(target);
-            Backoff b;
+            Backoff b(&hdr->error_flags);
             for (;;) {
                 const uint32_t w = state_load(p);
                 const uint32_t s = sget(w);
@@ -792,7 +800,7 @@ struct HeapCta {
                 if (cur != 1 && sget(state_load(st(target))) == kMarked) {
                     act = kShip;
                 } else if (next == target) {
-                    Backoff b;
+                    Backoff b(&hdr->error_flags);
                     for (;;) {
                         const uint32_t w = state_load(st(target));
                         if (sget(w) == kTarget) {
@@ -808,7 +816,7 @@ struct HeapCta {
                         }
                     }
                 } else {
-                    Backoff b;
+                    Backoff b(&hdr->error_flags);
                     for (;;) {
                         const uint32_t w = state_load(st(next));
                         const uint32_t s = sget(w);
@@ -877,7 +885,7 @@ struct HeapCta {
 
     // abandon_park (heap.cpp:393-407).  Calling lane only.
     __device__ void lane_abandon_park(unsigned long long slot) {
-        Backoff b;
+        Backoff b(&hdr->error_flags);
         uint32_t* p = st(slot);
         for (;;) {
             const uint32_t w = state_load(p);
@@ -952,7 +960,7 @@ struct HeapCta {
                         sh->ok[0] = 2;  // held, nothing to validate
                     } else {
                         uint32_t* pp = st(parent);
-                        Backoff b;
+                        Backoff b(&hdr->error_flags);
                         uint32_t w;
                         for (;;) {
                             w = state_load(pp);
@@ -990,7 +998,7 @@ struct HeapCta {
             for (;;) {
                 if (leader()) {
                     uint32_t* pc = st(cur);
-                    Backoff b;
+                    Backoff b(&hdr->error_flags);
                     uint32_t owned = 0;
                     for (;;) {
                         const uint32_t w = state_load(pc);
@@ -1097,7 +1105,7 @@ struct HeapCta {
                         sh->ok[0] = 2;
                     } else {
                         uint32_t* pp = st(parent);
-                        Backoff b;
+                        Backoff b(&hdr->error_flags);
                         uint32_t w;
                         for (;;) {
                             w = state_load(pp);
@@ -1138,7 +1146,7 @@ struct HeapCta {
                     // word unknown (a combiner claimed the target): poll it
                     uint32_t* pc = st(cur);
                     uint32_t w;
-                    Backoff b;
+                    Backoff b(&hdr->error_flags);
                     while (sget(w = state_load(pc)) != kInsHold) { b.pause(); BH_WAIT_NOTE(__LINE__); }
                     retake_ok = state_cas(pc, w, swith(w, kInUse));
                     cur_word = swith(w, kInUse);
@@ -1217,7 +1225,7 @@ struct HeapCta {
                 uint32_t claim = 0, w = 0;
                 if (slot <= hv.slot_count) {
                     uint32_t* p = st(slot);
-                    Backoff b;
+                    Backoff b(&hdr->error_flags);
                     for (;;) {
                         w = state_load(p);
                         const uint32_t s = sget(w);
@@ -1280,7 +1288,7 @@ struct HeapCta {
     enum { kTake = 1, kCoop = 2 };
     __device__ void lane_poll_last(unsigned long long last) {
         uint32_t* p = st(last);
-        Backoff b;
+        Backoff b(&hdr->error_flags);
         for (;;) {
             const uint32_t w = state_load(p);
             const uint32_t s = sget(w);
@@ -1291,7 +1299,7 @@ struct HeapCta {
                 return;
             }
             if (s == kTarget && state_cas(p, w, swith(w, kMarked))) {
-                Backoff wb;
+                Backoff wb(&hdr->error_flags);
                 while (sget(state_load(p)) != kAvail) { wb.pause(); BH_WAIT_NOTE(__LINE__); }
                 sh->act = kCoop;
                 return;
@@ -1849,7 +1857,7 @@ struct HeapCta {
                     w = guess;
                 } else if (slot <= hv.slot_count) {
                     uint32_t* p = st(slot);
-                    Backoff b;
+                    Backoff b(&hdr->error_flags);
                     for (;;) {
                         w = state_poll(p);  // relaxed poll + acquire fence (no L1 invalidation per poll)
                         const uint32_t s = sget(w);
@@ -1902,7 +1910,7 @@ struct HeapCta {
                 act = kTake;
                 w = guess;
             } else if (lane == 0) {
-                Backoff b;
+                Backoff b(&hdr->error_flags);
                 for (;;) {
                     w = state_poll(p);
                     const uint32_t s = sget(w);
@@ -1912,7 +1920,7 @@ struct HeapCta {
                         break;
                     }
                     if (s == kTarget && state_cas(p, w, swith(w, kMarked))) {
-                        Backoff wb;
+                        Backoff wb(&hdr->error_flags);
                         while (sget(state_load(p)) != kAvail) wb.pause();
                         act = kCoop;
                         break;

@@ -77,6 +77,7 @@ enum ErrorFlag : unsigned long long {
     kErrInteriorEmpty = 1ull << 1,    // heap.cpp:286 assert
     kErrEventOverflow = 1ull << 2,
     kErrRetake = 1ull << 3,           // gated BU climb: re-take CAS of the parked slot failed
+    kErrStuck = 1ull << 4,            // a spin wait passed ~4 s (deadlock watchdog, workload.cpp:22-53)
 };
 
 // kEvAcqRefill: acquire of a delete's refill source (refill_root_from,

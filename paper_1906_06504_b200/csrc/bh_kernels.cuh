@@ -20,9 +20,13 @@ __global__ void __launch_bounds__(T) sort_rows_kernel(Key* keys, const uint32_t*
     for (unsigned long long row = blockIdx.x; row < rows; row += gridDim.x) {
         Key* g = keys + row * K;
         const uint32_t n = lens ? lens[row] : (uint32_t)K;
-        for (uint32_t i = threadIdx.x; i < (uint32_t)K; i += T) s[i] = i < n ? g[i] : KeyLimits<Key>::kMax;
-        __syncthreads();
-        cta_bitonic_sort<Key, K, T>(s);
+        if constexpr (K >= T) {
+            cta_sort_batch<Key, K, T>(g, n, s, s + K);  // (callers validated the keys)
+        } else {
+            for (uint32_t i = threadIdx.x; i < (uint32_t)K; i += T) s[i] = i < n ? g[i] : KeyLimits<Key>::kMax;
+            __syncthreads();
+            cta_bitonic_sort<Key, K, T>(s);
+        }
         cta_store<Key, T>(g, s, K);
         __syncthreads();
     }
@@ -145,10 +149,15 @@ int kernel_info_k(KernelInfo* info) {
 template <typename Key, int K>
 int launch_sort_k(void* keys, const uint32_t* lens, uint64_t rows, cudaStream_t stream) {
     using Cfg = KernelCfg<Key, K>;
-    const uint32_t smem = K * sizeof(Key);
+    const uint32_t smem = 2 * K * sizeof(Key);  // ping-pong pair of cta_sort_batch
     const unsigned long long cap = 16ull * device_sm_count();
     const unsigned grid = (unsigned)(rows < cap ? rows : cap);
     if (grid == 0) return BH_OK;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(sort_rows_kernel<Key, K, Cfg::kThreads>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return note_cuda(e);
+    }
     sort_rows_kernel<Key, K, Cfg::kThreads>
         <<<grid, Cfg::kThreads, smem, stream>>>(static_cast<Key*>(keys), lens, rows);
     return note_cuda(cudaGetLastError());

@@ -85,3 +85,30 @@ def test_config_errors_are_raised_before_device_use():
         P.GeneralizedHeap(P.Variant.TD, 4, 0)
     with pytest.raises(P.ConfigError):
         P.GeneralizedHeap(P.Variant.TD, 4, 16, key_bits=16)
+
+
+@pytest.mark.gpu
+def test_run_watchdog_reports_a_run_past_its_deadline():
+    """bh_run_ops waits with a deadline (BH_RUN_TIMEOUT_S), the host half of
+    the reference's deadlock watchdog (proj/src/workload.cpp:22-53): a run
+    still going when it expires returns BH_E_INTERNAL instead of blocking."""
+    import numpy as np
+    from oracle import oracle as O
+    from paper_1906_06504_b200 import GeneralizedHeap, Variant, phase_ops
+    k, n = 1024, 1 << 22
+    keys = O.generate_keys(n, 5).astype(np.uint32)
+    heap = GeneralizedHeap(Variant.BU, k, n // k + 64, key_bits=32)
+    old = os.environ.get("BH_RUN_TIMEOUT_S")
+    os.environ["BH_RUN_TIMEOUT_S"] = "0.000001"
+    try:
+        with pytest.raises(Exception, match="watchdog"):
+            heap.run_ops(phase_ops(0, n, k), keys, 0)
+    finally:
+        if old is None:
+            del os.environ["BH_RUN_TIMEOUT_S"]
+        else:
+            os.environ["BH_RUN_TIMEOUT_S"] = old
+    # the run itself finishes; the heap is whole afterwards
+    d = heap.run_ops(phase_ops(1, n, k), np.zeros(0, np.uint32), n)
+    out = d.out.reshape(-1, k)[np.argsort(d.seq, kind="stable")].reshape(-1).astype(np.uint64)
+    assert np.array_equal(out, O.sort_u64(keys))

@@ -2,7 +2,14 @@
 step as proj/src/heap.cpp writes it (insert :123-188 + insert_bu :295-407,
 do_delete :420-465 + refill :467-531 + heapify :547-667).  Every shared
 read, CAS and write is a scheduling point.  Checks property 1 and multiset
-conservation at quiescence.  Diagnostic only."""
+conservation at quiescence.  Diagnostic only (tests/test_bu_gate_model.py
+runs it).
+
+GATE=True adds the BU phase gate of the CUDA heap (bh_heap.cuh gate_try /
+gate_wait, DESIGN.md section 4 item 2) in its simplest form: under the root
+lock, an insert that will climb (rank >= 2) waits while a delete heapify is
+in flight, and a delete that will heapify (>= 2 nodes) waits while a climb is
+in flight; a waiter lets the root go and queues again."""
 import random
 import sys
 
@@ -12,6 +19,7 @@ SENT = float("inf")
 
 TAGS = True
 RECHECK = True
+GATE = False
 
 
 def S(v):
@@ -24,6 +32,8 @@ class Heap:
         self.st = [AVAIL] * (slots + 1)
         self.nd = [SENT] * (slots + 1)
         self.count = 0
+        self.climbers = 0
+        self.deleters = 0
 
     def cas(self, i, exp, new):
         if self.st[i] == exp or (not TAGS and S(self.st[i]) == S(exp) and exp < 8):
@@ -50,10 +60,39 @@ def lock_avail(h, i):
 _tag = [0]
 
 
-def insert(h, key, log):
+def gated(h, body, climb):
+    """Run an op body behind the phase gate (root taken here)."""
+    while True:
+        yield from lock_avail(h, 1)
+        yield
+        needs = (h.count + 1 >= 2) if climb else (h.count >= 2)
+        other = h.deleters if climb else h.climbers
+        if needs and other > 0:
+            yield
+            h.st[1] = AVAIL
+            continue
+        break
+    if needs:
+        if climb:
+            h.climbers += 1
+        else:
+            h.deleters += 1
+    yield from body
+    if needs:
+        if climb:
+            h.climbers -= 1
+        else:
+            h.deleters -= 1
+
+
+def insert(h, key, log, root_held=False):
+    if GATE and not root_held:
+        yield from gated(h, insert(h, key, log, True), True)
+        return
     _tag[0] += 1
     tag = _tag[0] if TAGS else 0
-    yield from lock_avail(h, 1)
+    if not root_held:
+        yield from lock_avail(h, 1)
     yield
     rank = h.count + 1
     h.count = rank
@@ -164,8 +203,12 @@ def acquire_child(h, slot):
     return (slot, True, h.nd[slot] == SENT, rel)
 
 
-def delete(h, log):
-    yield from lock_avail(h, 1)
+def delete(h, log, root_held=False):
+    if GATE and not root_held:
+        yield from gated(h, delete(h, log, True), False)
+        return
+    if not root_held:
+        yield from lock_avail(h, 1)
     yield
     nodes = h.count
     if nodes == 0:
@@ -281,8 +324,9 @@ def run(seed, workers=6, ops=40, slots=255):
 
 if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
-    TAGS = len(sys.argv) < 3 or sys.argv[2] != "notags"
+    TAGS = "notags" not in sys.argv[2:]
     RECHECK = TAGS
+    GATE = "gate" in sys.argv[2:]
     fails = 0
     for seed in range(n):
         bad, ms = run(seed)
