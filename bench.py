@@ -235,14 +235,18 @@ def root_service(a, dev, keys, stream, flush, value):
     ghz = 1.965  # B200 SM clock under load (the clocks sampled above)
     us = lambda c, m: c / max(m, 1) / (ghz * 1e3)
     t_ins = us(p_ins["ins_root_hold"], p_ins["ins_ops"])
+    # served ops: the server's own (counted in del_ops, one per hold) and
+    # the waiters it served (del_served); the rest held the root themselves
     served = p["del_served"] + p["del_serve_holds"]
+    unserved = max(p["del_ops"] - p["del_serve_holds"], 0)
     sv = sum(p[f] for f in ("sv_split", "sv_r1", "sv_r2", "sv_r3", "sv_next"))
     t_del_served = us(sv, served)
-    t_del_plain = us(p["del_root_hold"], p["del_ops"] - served)
-    t_del = (served * t_del_served + (p["del_ops"] - served) * t_del_plain) / max(p["del_ops"], 1)
+    t_del_plain = us(p["del_root_hold"], unserved)
+    t_del = (served * t_del_served + unserved * t_del_plain) / max(served + unserved, 1)
     bound = 2 * n / (n_ops * (t_ins + t_del) * 1e-6)
     return {"t_root_insert_us": t_ins, "t_root_delete_us": t_del,
-            "deletes_served": served, "delete_ops": p["del_ops"],
+            "t_serve_per_delete_us": t_del_served, "t_root_hold_unserved_delete_us": t_del_plain,
+            "deletes_served": served, "deletes_unserved": unserved,
             "bound_key_ops_per_s": bound, "achieved_frac_of_bound": value / bound,
             "source": "one BH_FLAG_PROFILE step outside the timed region: mean root hold per insert "
                       "(combining holds included) + per-op delete-server service time"}
