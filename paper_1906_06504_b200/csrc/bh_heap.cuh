@@ -233,6 +233,7 @@ struct HeapCta {
     Key* bufs;
     unsigned long long cnt[kNumCounters];
     unsigned long long cur_op;
+    uint32_t sv_j = 0;  // delete server: the op's index in the hold (timeline)
     bool elide;
     static constexpr bool record = Rec;
     bool prof;
@@ -1390,6 +1391,8 @@ struct HeapCta {
     static constexpr uint32_t kRefBase = T >= 256 ? 64 : 32;  // refill group: [kRefBase, T/2)
     static constexpr uint32_t kHalfT = T / 2;
     static constexpr uint32_t kPubLane = T >= 256 ? 32 : 1;  // outside the refill group
+    // warp 0 claims hi1's children at the op's start (needs warp 1 for kPubLane)
+    static constexpr bool kEarlyClaim = T >= 256;
 
     __device__ __forceinline__ Key* mbox(unsigned long long t) const {
         return static_cast<Key*>(hv.mailbox) + (t % kRootQueue) * (unsigned long long)K;
@@ -1476,12 +1479,9 @@ struct HeapCta {
                                             unsigned long long nodes, unsigned long long t, int& n1, int& n2,
                                             int& n3, int& cbuf, uint32_t& crel, uint32_t pre_w) {
         const unsigned long long ts0 = now();
+        const uint32_t jj = sv_j;  // the op's index in the hold (timeline)
+        if (leader()) tl(jj, 0);
         Key* out = static_cast<Key*>(rv.out_pool) + off;
-        if (threadIdx.x >= kHalfT) {  // the result: the root's k keys (B group: no fences follow)
-            const uint4* sv = reinterpret_cast<const uint4*>(buf(n1));
-            uint4* gv = reinterpret_cast<uint4*>(out);
-            for (uint32_t i = threadIdx.x - kHalfT; i < kNodeBytes / 16; i += kHalfT) __stcg(gv + i, sv[i]);
-        }
         count(cDeletes);
         if (leader() && buf(n1)[K - 1] == kMaxKey)
             atomicOr(&hdr->error_flags, (unsigned long long)kErrSentinelEscaped);
@@ -1524,13 +1524,22 @@ struct HeapCta {
         // H0 and lo0, then the claim of hi1's children.  Warps below kRefBase
         // stay out of both groups: the leader's bookkeeping and kPubLane's
         // flush of the previous op + next-waiter lookup run beside them.
-        if (threadIdx.x < kRefBase) {
+        if (threadIdx.x < 32 && kEarlyClaim) {
+            // warp 0: hi1's children (level 2), claimed and loaded at the
+            // op's start beside H0 || lo0 and the refill (hi1 is known from
+            // nodes 2-3 alone); the one claim the server may wait on
+            const unsigned long long tc = now();
+            acquire_children(hi1, buf(l2), buf(r2), 0, 32, 3);
+            if (threadIdx.x == 0) tl(jj, 5);
+            if (prof && threadIdx.x == 0) atomicAdd(&hv.prof[pfSvClaim], now() - tc);
+        } else if (threadIdx.x < kRefBase) {
             // (a look-up beside the flush instead of after it -- three lanes,
             // three chains -- hung mixed insert/delete runs with serving at
             // full size, tools/gpu/bisect_mixed.sh; the order below is the
             // tested one)
             if (threadIdx.x == kPubLane) {
                 sv_flush(sh->pd);
+                tl(jj, 1);
                 unsigned long long nop = 0;
                 const bool more = nodes - 1 >= kServeMin && waiting_delete(t + 1, nop);
                 sh->serve = more;
@@ -1539,10 +1548,12 @@ struct HeapCta {
                     sh->off_next = rv.ops[nop].offset;
                     sh->next_w = state_load(st(slot_for_rank(nodes - 1)));  // the next op's refill
                 }
+                tl(jj, 2);
             }
         } else if (threadIdx.x < kHalfT) {
             // released here, before the server waits on any claim (below)
             refill_last(last, buf(rf), kRefBase, kHalfT - kRefBase, 1, pre_w);
+            if (threadIdx.x == kRefBase) tl(jj, 3);
             if (prof && threadIdx.x == kRefBase) atomicAdd(&hv.prof[pfSvA], now() - ts0);
         } else {
             // both halves of merge(L, R): H0 and the lo child's new batch,
@@ -1557,12 +1568,28 @@ struct HeapCta {
                 if (bw < (uint32_t)kQ) grp_merge_half<Key, K, kQ, false, false>(L, R, buf(h0), bw);
                 else grp_merge_half<Key, K, kQ, true, false>(L, R, buf(nlo), bw - kQ);
             }
+            if (threadIdx.x == kHalfT) tl(jj, 4);
             if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvB], now() - ts0);
-            const unsigned long long tc = now();
-            acquire_children(hi1, buf(l2), buf(r2), kHalfT, kHalfT, 2);
-            if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvClaim], now() - tc);
+            if constexpr (!kEarlyClaim) {
+                const unsigned long long tc = now();
+                acquire_children(hi1, buf(l2), buf(r2), kHalfT, kHalfT, 2);
+                if (threadIdx.x == kHalfT) tl(jj, 5);
+                if (prof && threadIdx.x == kHalfT) atomicAdd(&hv.prof[pfSvClaim], now() - tc);
+            }
         }
+        // (timeline stamps are taken where a warp *reaches* a barrier: a
+        // clock read right after BAR.SYNC.DEFER_BLOCKING issues before the
+        // warp blocks, tools/microbench/mb_barmix.cu)
+        if (threadIdx.x == kHalfT + 32) tl(jj, 6);
         __syncthreads();
+        // the result (the root's k keys), written after the split: stores
+        // issued at the op's start would sit in front of kPubLane's fence,
+        // which publishes the previous op's continuation (the chain)
+        {
+            const uint4* sv = reinterpret_cast<const uint4*>(buf(n1));
+            uint4* gv = reinterpret_cast<uint4*>(out);
+            for (uint32_t i = threadIdx.x; i < kNodeBytes / 16; i += T) __stcg(gv + i, sv[i]);
+        }
         const unsigned long long ts1 = now();
         pf_add(pfSvSplit, ts1 - ts0);
         const bool handoff = sh->serve != 0;
@@ -1600,7 +1627,10 @@ struct HeapCta {
             ca = rf;
         }
         pf_add(pfSvR1, now() - ts1);
-        __syncthreads();
+        // (a CTA barrier costs ~250-450 cycles here: none when the round
+        // wrote nothing -- the refill moved down unchanged)
+        if (mcur0) __syncthreads();
+        if (leader()) tl(jj, 7);
         const unsigned long long ts2 = now();
 
         // ---- level 1: cur = carried batch at hi1, children claimed above ----
@@ -1645,6 +1675,7 @@ struct HeapCta {
                 __syncthreads();
             }
             const unsigned long long ts3 = now();
+            if (leader()) tl(jj, 8);
             pf_add(pfSvR2, ts3 - ts2);
             const int hd1 = mc1 ? h1 : (hl1 ? l2 : r2);
             const bool mcur1 = !(elide && !needs_merge_full<Key, K>(CA, buf(hd1)));
@@ -1669,7 +1700,9 @@ struct HeapCta {
             crel = hi2_rel;
             pf_add(pfSvR3, now() - ts3);
         }
-        __syncthreads();
+        // (no barrier here: serve_deletes' loop barrier, before the next op
+        // or the write-back, orders this round's writes)
+        if (leader()) tl(jj, 9);
         n1 = nr;
         if (hi1 == 2) {
             n2 = nhi;
@@ -1696,8 +1729,12 @@ struct HeapCta {
             sh->pd.n = 0;
             sh->pd.pub = 0;
         }
+        sv_j = 0;
+        if (prof && threadIdx.x == 0)
+            for (uint32_t i = 0; i < kTlSmemOps * 24u; ++i) sh->tl[i] = 0;
+        __syncthreads();
 
-        for (;;) {
+        for (;; ++sv_j) {
             cur_op = op;  // the lock events of this op's top levels are its own
             if (record && served && leader()) {  // the first op holds 1-3 already
                 rec(kEvAcq, 1);
@@ -1718,6 +1755,7 @@ struct HeapCta {
             const unsigned long long noff = sh->off_next;
             pre_w = sh->next_w;  // the next op's refill word, observed in this op
             __syncthreads();  // everyone has read sh->serve / op_next
+            if (leader()) tl(sv_j, 10);
             if (!more) break;
             // the waiter of ticket t+1 takes this op's continuation (its
             // carried batch is in mbox(t+1)); its own op is served next.  The
@@ -1734,6 +1772,9 @@ struct HeapCta {
             ++served;
             pf_add(pfSvNext, now() - tn);
         }
+        if (prof)  // the timeline (first hold of the run only)
+            for (uint32_t i = threadIdx.x; i < kTlSmemOps * 24u; i += T)
+                if (sh->tl[i]) atomicCAS(&hv.prof[kTlBase + (i / 24u) * 32u + i % 24u], 0ull, sh->tl[i]);
         // write the top levels back, then release everything and the root
         cta_store<Key, T>(node(1), buf(n1), K);
         cta_store<Key, T>(node(2), buf(n2), K);

@@ -61,6 +61,21 @@ __global__ void sync_bench(int mode, int iters, unsigned long long* out, uint4* 
             }
         } else if (mode == 10) {  // mbarrier test_wait on a completed phase
             if (w == 0) acc += mb_test(&mb[0], 0);
+        } else if (mode == 11) {  // __threadfence with no stores outstanding
+            if (w == 0) __threadfence();
+        } else if (mode == 12) {  // 4 KiB st.cg by the warp, then __threadfence by lane 0
+            if (w == 0) {
+                for (int i = lane; i < 256; i += 32) __stcg(g + i + 256 * (it & 7), make_uint4(it, 1, 2, 3));
+                __syncwarp();
+                if (lane == 0) __threadfence();
+                __syncwarp();
+            }
+        } else if (mode == 13) {  // 4 KiB st.cg by 8 warps, CTA barrier, __threadfence by thread 0
+            if (w < 8)
+                for (int i = threadIdx.x; i < 256; i += 256) __stcg(g + i + 256 * (it & 7), make_uint4(it, 1, 2, 3));
+            __syncthreads();
+            if (threadIdx.x == 0) __threadfence();
+            __syncthreads();
         } else if (mode == 6) {
             if (w == 0) {
                 for (int i = lane; i < 256; i += 32) __stcg(g + i, make_uint4(it, 1, 2, 3));
@@ -80,8 +95,10 @@ int main() {
     const char* names[] = {"try_wait on a completed phase", "arrive.release, no stores", "4 KiB st.cg + arrive.release",
                            "4 KiB st.cg + arrive.relaxed", "named barrier x12 warps", "named barrier after 4 KiB st.cg",
                            "4 KiB st.cg + clock read", "bar.sync (aligned) x12 warps", "__syncthreads x16 warps",
-                           "volatile smem flag (set) + fence.cta", "test_wait on a completed phase"};
-    for (int m = 0; m <= 10; ++m) {
+                           "volatile smem flag (set) + fence.cta", "test_wait on a completed phase",
+                           "__threadfence, nothing outstanding", "4 KiB st.cg + __threadfence (warp)",
+                           "4 KiB st.cg (8 warps) + bar + fence + bar"};
+    for (int m = 0; m <= 13; ++m) {
         sync_bench<<<1, 512>>>(m, 2000, o, g);
         CK(cudaDeviceSynchronize());
         unsigned long long c;
