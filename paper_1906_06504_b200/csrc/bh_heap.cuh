@@ -1127,6 +1127,7 @@ struct HeapCta {
                 if (leader() && sh->ok[0] == 0) sh->ok[0] = ok;
                 __syncthreads();
                 if (sh->ok[0]) break;
+                __syncthreads();  // (a retry: everyone has read sh->ok before the leader rewrites it)
             }
             uint32_t parent_word = 0;
             if (leader() && parent != 1) {

@@ -1,7 +1,8 @@
 """The reference's knapsack_bb (oracle/_ref, unmodified sources) on every
 golden knapsack instance, one child process each (arena exhaustion calls
 std::terminate in the reference).  Writes tests/golden/knapsack_ref_bb.json:
-per instance the optimum/explored/seconds, or the failure."""
+per instance the optimum/explored/seconds, or the failure.
+usage: ref_knapsack_table.py [WORKERS] [TIMEOUT_S] [OUT_JSON]"""
 import json
 import os
 import sys
@@ -20,5 +21,5 @@ for c in gold:
     r["workers"] = workers
     out.append(r)
     print(r, flush=True)
-path = os.path.join(ROOT, "tests", "golden", f"knapsack_ref_bb_w{workers}.json")
+path = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "tests", "golden", f"knapsack_ref_bb_w{workers}.json")
 json.dump({"generator": "tools/ref_knapsack_table.py", "timeout_s": timeout, "cases": out}, open(path, "w"), indent=0)
