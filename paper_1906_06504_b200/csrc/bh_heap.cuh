@@ -1554,6 +1554,12 @@ struct HeapCta {
         } else if (threadIdx.x < kHalfT) {
             // released here, before the server waits on any claim (below)
             refill_last(last, buf(rf), kRefBase, kHalfT - kRefBase, 1, pre_w);
+            // the refill batch usually moves down levels 0-1 unchanged and is
+            // then the carried batch this op hands to the next ticket: into
+            // its mailbox now, long before the next op's publishing fence
+            // (overwritten in round 3 when it is not; unread when the hold
+            // ends)
+            grp_store<Key>(mbox(t + 1), buf(rf), K, threadIdx.x - kRefBase, kHalfT - kRefBase);
             if (threadIdx.x == kRefBase) tl(jj, 3);
             if (prof && threadIdx.x == kRefBase) atomicAdd(&hv.prof[pfSvA], now() - ts0);
         } else {
@@ -1694,7 +1700,7 @@ struct HeapCta {
             } else {
                 nhi = hd1;
                 cbuf = ca;
-                if (handoff) cta_store<Key, T>(mbox(t + 1), CA, K);
+                if (handoff && ca != rf) cta_store<Key, T>(mbox(t + 1), CA, K);
             }
             if (lo2_locked) pend(lo2, lo2_rel);  // merged above, or unchanged
             cont = hi2;
