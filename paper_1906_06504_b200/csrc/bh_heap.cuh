@@ -509,6 +509,10 @@ struct HeapCta {
     // the first of them flips the phase and its whole batch enters.  Leader
     // lane, root held.  Returns true when the op may start (counted).
     __device__ bool gate_try(bool climb) {
+        if (hv.flags & kDbgNoGate) {  // measurement only: what the gate costs
+            atomicAdd(gate_mine(climb), 1ull);
+            return true;
+        }
         const unsigned long long me = climb ? 0ull : 1ull;
         const unsigned long long ph = ld_cg_u64(&hdr->gate_phase);
         const unsigned long long closing = ld_cg_u64(&hdr->gate_closing);
