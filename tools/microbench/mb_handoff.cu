@@ -184,6 +184,47 @@ __global__ void __launch_bounds__(512, 1) handoff(Args a) {
     if (me == 0 && tid < 256) atomicAdd(a.out + 3, (unsigned long long)buf[tid].z);
 }
 
+
+// Node loads inside one CTA (L2-resident source, as the heap's nodes are):
+// n nodes of 4 KiB into shared memory, then a CTA barrier.  mode 0: ld.cg
+// uint4 loop (the heap's cta_load); 1: cp.async.cg 16 B (LDGSTS) + wait_all;
+// 2: one cp.async.bulk per node issued by one thread, mbarrier complete_tx.
+__global__ void __launch_bounds__(512, 1) node_load(int mode, int n, int iters, const uint4* g,
+                                                    unsigned long long* out) {
+    __shared__ __align__(128) uint4 buf[3 * 256];
+    __shared__ __align__(8) unsigned long long mb;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mb)) : "memory");
+    __syncthreads();
+    unsigned long long acc = 0, t0 = 0;
+    for (int it = -8; it < iters; ++it) {
+        if (it == 0) t0 = clk();
+        const uint4* src = g + (it & 7) * 3 * 256;  // 8 rotating L2-resident node triples
+        if (mode == 0) {
+            for (uint32_t i = tid; i < 256u * n; i += 512) buf[i] = __ldcg(src + i);
+        } else if (mode == 1) {
+            for (uint32_t i = tid; i < 256u * n; i += 512)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(buf + i)), "l"(src + i) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        } else {
+            if (tid == 0) {
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mb)), "r"(4096 * n) : "memory");
+                for (int j = 0; j < n; ++j)
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 4096, [%2];"
+                                 ::"r"(su32(buf + 256 * j)), "l"(src + 256 * j), "r"(su32(&mb)) : "memory");
+                wait_parity(su32(&mb), (uint32_t)((it + 8) & 1), false);
+            }
+        }
+        __syncthreads();
+        acc += buf[(tid * 7) % (256 * n)].x;  // consume
+        __syncthreads();
+    }
+    unsigned long long t1 = clk();
+    if (tid == 0) out[0] = (t1 - t0) / iters;
+    if (acc == 12345) out[1] = acc;
+}
+
 int main() {
     unsigned long long* o;
     uint4* mbox;
@@ -226,5 +267,17 @@ int main() {
                    cl ? "cluster2" : "no-cluster", h[1], h[2], h[0], h[3] == want ? "ok" : "MISMATCH");
         }
     }
+    uint4* g;
+    CK(cudaMalloc(&g, 8 * 3 * 4096));
+    CK(cudaMemset(g, 1, 8 * 3 * 4096));
+    const char* lnames[] = {"ld.cg uint4 loop", "cp.async.cg 16 B (LDGSTS)", "cp.async.bulk (TMA 1-D)"};
+    for (int n = 1; n <= 3; ++n)
+        for (int mode = 0; mode <= 2; ++mode) {
+            node_load<<<1, 512>>>(mode, n, 2000, g, o);
+            CK(cudaDeviceSynchronize());
+            unsigned long long c;
+            CK(cudaMemcpy(&c, o, 8, cudaMemcpyDeviceToHost));
+            printf("load %d x 4 KiB %-28s : %5llu cycles (incl. 2 CTA barriers)\n", n, lnames[mode], c);
+        }
     return 0;
 }
