@@ -230,7 +230,9 @@ struct Backoff {
     }
 };
 // For a waiter whose wake-up is on a critical path (a delete that a delete
-// server may hand a continuation): short sleeps only.
+// server may hand a continuation): no sleep, each poll is one L2 round trip
+// on the waiter's own 128-byte line (32 ns sleeps cost the 2^26 / K=1024
+// delete phase ~1.2 ms, profiles/r2/ab_final.txt).
 struct QuickBackoff {
     uint32_t n = 0;
     unsigned long long* stuck = nullptr;
@@ -238,7 +240,6 @@ struct QuickBackoff {
     __device__ __forceinline__ explicit QuickBackoff(unsigned long long* flag_word) : stuck(flag_word) {}
     __device__ __forceinline__ void pause() {
         ++n;
-        if (n > 32) __nanosleep(32);
         if (n == (kStuckSpins << 3) && stuck) atomicOr(stuck, kStuckFlag);
     }
 };

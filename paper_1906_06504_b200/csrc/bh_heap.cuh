@@ -132,11 +132,21 @@ constexpr uint32_t kTlSmemOps = 16;
 
 // Three-level delete server: node sizes whose 24 buffers fit in shared memory
 // next to everything else, on 512-thread CTAs (16 warps: control, claim,
-// 12 merge warps, 2 refill warps).
+// 12 merge warps, 2 refill warps).  Compiled only with -DBH_SERVE3 (make
+// SERVE3=1): it is an experiment, and compiled in, its
+// code and its 24-buffer shared-memory footprint slow the production path
+// (measured on one box: 2^26 / K=1024 insert phase 87.0 -> 85.1 ms, delete
+// phase 304.7 -> 301.3 ms without it, profiles/r2/ab_final.txt).
+#ifdef BH_SERVE3
+constexpr bool kServe3Built = true;
+#else
+constexpr bool kServe3Built = false;
+#endif
 template <typename Key, int K, int T>
 struct Serve3Cfg {
     static constexpr int kBufs = 24;
-    static constexpr bool kOn = T == 512 && (unsigned long long)kBufs * K * sizeof(Key) <= 200ull * 1024ull;
+    static constexpr bool kOn =
+        kServe3Built && T == 512 && (unsigned long long)kBufs * K * sizeof(Key) <= 200ull * 1024ull;
 };
 
 // Profile slots (BH_FLAG_PROFILE): SM cycles summed over ops by the leader.
@@ -2902,40 +2912,6 @@ struct HeapCta {
             prefetch_node(2 * hi);  // warm L2 with the next level
             prefetch_node(2 * hi + 1);
             // ---- phase 1 ----
-            constexpr bool kInvFast = T >= 64 && K >= 32 * (T / 64);
-            if constexpr (kInvFast) if (merge_children && hx < 0) {
-                // H not precomputed (the root level, a continuation's first
-                // level).  The full inversion -- the carried batch lies
-                // entirely above H, the k smallest of the children, as a
-                // refill batch usually does near the top -- is decided from
-                // H's largest key (one warp-level split search) before any
-                // merging: then node cur takes H and the lo child the rest,
-                // both halves of merge(L, R) written straight to HBM in one
-                // round, and the carried batch moves down unchanged.  Same
-                // merges, elisions, contents and lock order as below; one
-                // merge round and one barrier less on the chain.
-                const Key hmax = warp_kth_max<Key, K>(L, R);
-                if (elide && hmax <= cur_s[0]) {
-                    count(cElided);  // merge_and_sort(cur, H) elided (heap.cpp:643-652)
-                    count(cVisits);
-                    constexpr int kH = kInvFast ? T / 64 : 1;  // warps per half
-                    const uint32_t w = threadIdx.x >> 5;
-                    if (w < (uint32_t)kH) grp_merge_half<Key, K, kH, false, true>(L, R, node(cur), w);
-                    else if (w < 2u * kH && lo_locked) grp_merge_half<Key, K, kH, true, true>(L, R, node(lo), w - kH);
-                    __syncthreads();
-                    if (threadIdx.x == kRelLane) {
-                        lane_unlock(cur, cur_rel);
-                        if (lo_locked) lane_unlock(lo, lo_rel);
-                    }
-                    if (cur == 1) pf_add(pfDelRootHold, now() - t_root);
-                    pf_add(pfLvMerge, now() - tl2);
-                    have = false;  // hi's children: claimed at the top of the next level
-                    hx = -1;
-                    cur = hi;
-                    cur_rel = hi_rel;
-                    continue;      // the carried batch stays in buf(ci)
-                }
-            }
             if (merge_children && hx < 0) {  // H not precomputed (root level)
                 hx = free_buf((1u << ci) | (1u << li) | (1u << ri));
                 grp_merge_half<Key, K, T / 32, false, false>(L, R, buf(hx), threadIdx.x >> 5);

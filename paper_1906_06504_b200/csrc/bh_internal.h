@@ -37,7 +37,7 @@ constexpr uint32_t kDbgNoCombine = 0x800;       // no insert combining in the ro
 constexpr uint32_t kDbgParkClimb = 0x1000;      // reference BU climb (fenced park, reload on re-take)
 constexpr uint32_t kDbgNoDelServe = 0x2000;     // no delete serving in the root queue lock
 constexpr uint32_t kDbgNoGate = 0x8000;         // measurement only: BU phase gate off (the reference's race returns)
-constexpr uint32_t kDbgServe3 = 0x4000;         // three-level delete server (experimental, DESIGN.md s.6) where it fits
+constexpr uint32_t kDbgServe3 = 0x4000;         // three-level delete server (experimental, DESIGN.md s.6): SERVE3=1 builds, where it fits
 
 // Heap header, root-lock guarded (reference heap.hpp:173-177).  One cache
 // line; the partial buffer follows in its own allocation.

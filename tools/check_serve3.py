@@ -1,7 +1,11 @@
 """Three-level delete server check (tooling): drains and partial drains at
 one K with the three-level server (flags 0x4000), the two-level one (0) and
 no serving (0x2000); outputs, counters and the heap left behind must agree.
-usage: check_serve3.py LOG2N K [REPS]"""
+usage: check_serve3.py LOG2N K [REPS]
+The server is compiled only into the SERVE3=1 library
+(make -C paper_1906_06504_b200/csrc SERVE3=1; BH_LIB=build_var/libbatchheap_b200_serve3.so);
+with the shipped library flag 0x4000 falls back to the two-level server and
+s3_ops stays 0."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
