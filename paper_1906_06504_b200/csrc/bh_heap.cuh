@@ -396,7 +396,11 @@ struct HeapCta {
             v = (uint32_t)vv;
             sh->contw = (uint32_t)(vv >> 32);
         } else {
-            Backoff b(&hdr->error_flags);
+            // (no sleeps either: each waiter polls its own line, and the
+            // root hand-off is on the insert phase's chain -- 256 ns sleeps
+            // cost the 2^26 / K=1024 insert phase ~1.3 ms,
+            // profiles/r2/ab_final.txt)
+            QuickBackoff b(&hdr->error_flags);
             while (((v = state_load(f)) & ~1u) != granted) { b.pause(); BH_WAIT_NOTE(__LINE__); }
         }
         sh->root_tk = t;
