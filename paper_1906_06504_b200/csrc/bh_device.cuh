@@ -229,11 +229,11 @@ struct Backoff {
         if (n == kStuckSpins && stuck) atomicOr(stuck, kStuckFlag);
     }
 };
-// For a waiter whose wake-up is on a critical path (a root queue-lock waiter;
-// a delete that a delete
-// server may hand a continuation): no sleep, each poll is one L2 round trip
-// on the waiter's own 128-byte line (32 ns sleeps cost the 2^26 / K=1024
-// delete phase ~1.2 ms, profiles/r2/ab_final.txt).
+// For a waiter whose wake-up is on a critical path (a root queue-lock
+// waiter, e.g. a delete that a delete server may hand a continuation): no
+// sleep, each poll is one L2 round trip on the waiter's own 128-byte line
+// (32 ns sleeps cost the 2^26 / K=1024 delete phase ~1.2 ms,
+// profiles/r2/ab_final.txt).
 struct QuickBackoff {
     uint32_t n = 0;
     unsigned long long* stuck = nullptr;
