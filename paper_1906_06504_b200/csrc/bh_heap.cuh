@@ -311,6 +311,12 @@ struct HeapCta {
     __device__ __forceinline__ void pf_add(int idx, unsigned long long v) {
         if (prof && leader()) atomicAdd(&hv.prof[idx], v);
     }
+    // per-level climb profile: `what` 0 = steps, 1 = parent-claim cycles,
+    // 2 = claim-to-release cycles; `parent` = the slot claimed
+    __device__ __forceinline__ void pf_lv(uint32_t what, unsigned long long parent, unsigned long long v) {
+        if (prof && leader())
+            atomicAdd(&hv.prof[kLvBase + what * kLvLevels + (63u - (uint32_t)__clzll((long long)parent))], v);
+    }
     __device__ __forceinline__ void prefetch_node(unsigned long long slot) {
         if (slot > hv.slot_count) return;
         cta_prefetch_l2<T>(node(slot), kNodeBytes, kPfFirst);
@@ -468,6 +474,73 @@ struct HeapCta {
         return g;
     }
 
+    // insert_bu's own target claim and insert combining in one pass
+    // (unrecorded heaps; recorded ones log each step through the two calls
+    // above).  Warp 0, root held, partial buffer empty: lane 0 claims this
+    // op's target (rank), lanes 1..31 the targets of the queued BU full-batch
+    // inserts behind it (ranks rank+1.., in ticket order), with the look-ups
+    // (queue tail, request words, target state words) in one round of loads
+    // and the claims in one round of CASes; then the leader publishes the
+    // responses, the header and the hand-offs behind one fence and lets the
+    // root go.  Same ranks, targets, states, sequence numbers and FIFO
+    // hand-off as the claim + serve_inserts + root_unlock it replaces
+    // (heap.cpp:126-188, 295-308).  Sets cur_word on every lane.
+    __device__ void claim_and_serve(unsigned long long target, unsigned long long rank, unsigned long long seq,
+                                    uint32_t& cur_word) {
+        const uint32_t lane = threadIdx.x & 31u;
+        const unsigned long long mine = sh->root_tk;
+        const unsigned long long t = mine + lane;  // lane 0: this op's own ticket
+        uint32_t* f = qline(t);
+        const unsigned long long rk = rank + lane;
+        const bool fits = rk <= hv.max_nodes;  // lane 0: checked by do_insert
+        const unsigned long long tg = lane ? (fits ? slot_for_rank(rk) : 0ull) : target;
+        // round 1
+        unsigned long long tail = 0;
+        if (lane == 0) tail = ld_cg_u64(&hdr->root_tail);
+        const uint32_t req = (lane && fits) ? state_load(f + 1) : 0u;
+        const uint32_t tw = fits ? state_load(st(tg)) : 0u;
+        tail = __shfl_sync(0xFFFFFFFFu, tail, 0);
+        const bool ok = lane == 0 || (fits && t < tail && req == (((uint32_t)t << 1) | 1u));
+        const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
+        const uint32_t n = bad ? (uint32_t)__ffs(bad) - 1u : 32u;  // lanes [0, n) claim
+        // round 2: the claims
+        uint32_t got = 0;
+        if (lane < n) {
+            const uint32_t st0 = sget(tw);
+            if ((st0 == kAvail || st0 == kDelMod) && state_cas(st(tg), tw, swith(tw, kInUse))) {
+                BH_OWN(tg);
+                got = swith(tw, kInUse);
+            } else {
+                lane_claim(tg, (1u << kAvail) | (1u << kDelMod), &got);
+            }
+        }
+        cur_word = __shfl_sync(0xFFFFFFFFu, got, 0);
+        const uint32_t g = n - 1u;  // ops served
+        if (lane && lane < n) {
+            st_cg_u64(reinterpret_cast<unsigned long long*>(f + 4), rk);
+            st_cg_u64(reinterpret_cast<unsigned long long*>(f + 6), tg);
+            st_cg_u64(reinterpret_cast<unsigned long long*>(f + 8), seq + lane);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (g) {
+                st_cg_u64(&hdr->node_count, rank + g);
+                st_cg_u64(&hdr->root_seq, seq + 1 + g);
+                atomicAdd(gate_mine(true), (unsigned long long)g);
+                count(cCombined, g);
+                pf_add(pfServed, g);
+                pf_add(pfServeHolds, 1);
+            }
+            __threadfence();  // claims, responses, header and gate count before any hand-off
+            for (uint32_t i = 1; i <= g; ++i)
+                state_store_relaxed(qline(mine + i), ((uint32_t)(mine + i) << 1) | 1u);
+            const unsigned long long nt = mine + g + 1;  // root_unlock
+            sh->root_tk = mine + g;
+            state_store_relaxed(qline(nt), (uint32_t)nt << 1);
+        }
+        __syncwarp();
+    }
+
     // Non-root claim: wait for one of `accept` (bitmask of states), CAS it to
     // INUSE.  Returns the state it was claimed from.  Calling lane only.
     __device__ uint32_t lane_claim(unsigned long long slot, uint32_t accept, uint32_t* claimed_word = nullptr) {
@@ -523,14 +596,19 @@ struct HeapCta {
     // the first of them flips the phase and its whole batch enters.  Leader
     // lane, root held.  Returns true when the op may start (counted).
     __device__ bool gate_try(bool climb) {
+        return gate_try(climb, ld_cg_u64(&hdr->gate_phase), ld_cg_u64(&hdr->gate_closing),
+                        ld_cg_u64(gate_other(climb)));
+    }
+    // With the gate words already loaded under the root lock (phase and
+    // closing only change under it; the other kind's count only falls
+    // outside it, so an early read errs on the waiting side).
+    __device__ bool gate_try(bool climb, unsigned long long ph, unsigned long long closing,
+                             unsigned long long other) {
         if (hv.flags & kDbgNoGate) {  // measurement only: what the gate costs
             atomicAdd(gate_mine(climb), 1ull);
             return true;
         }
         const unsigned long long me = climb ? 0ull : 1ull;
-        const unsigned long long ph = ld_cg_u64(&hdr->gate_phase);
-        const unsigned long long closing = ld_cg_u64(&hdr->gate_closing);
-        const unsigned long long other = ld_cg_u64(gate_other(climb));
         if (ph == me && !closing) {
             atomicAdd(gate_mine(climb), 1ull);  // ordered before the root release
             return true;
@@ -646,9 +724,16 @@ struct HeapCta {
             for (;;) {
                 served = root_lock(false, combinable);
                 if (served) break;
+                // the header and (BU) the gate words in one round of loads
                 const unsigned long long nd = ld_cg_u64(&hdr->node_count);
                 const unsigned long long pl = ld_cg_u64(&hdr->partial_len);
                 const unsigned long long sq = ld_cg_u64(&hdr->root_seq);
+                unsigned long long gph = 0, gcl = 0, got = 0;
+                if (hv.variant == BH_BU) {
+                    gph = ld_cg_u64(&hdr->gate_phase);
+                    gcl = ld_cg_u64(&hdr->gate_closing);
+                    got = ld_cg_u64(gate_other(true));
+                }
                 sh->nodes = nd;
                 sh->plen = pl;
                 sh->seq = sq;
@@ -656,7 +741,7 @@ struct HeapCta {
                 const bool climbs = hv.variant == BH_BU && n + (uint32_t)pl >= (uint32_t)K && nd >= 1 &&
                                     nd < hv.max_nodes;
                 if (!climbs) break;
-                if (gate_try(true)) {
+                if (gate_try(true, gph, gcl, got)) {
                     gated = 1;
                     break;
                 }
@@ -927,7 +1012,9 @@ struct HeapCta {
         Key* par = bat == buf(4) ? buf(1) : buf(4);
         Key* cu = buf(5);
         uint32_t cur_word = 0;  // leader: exact state word of the held `cur` (0 = unknown)
-        if (!served) {
+        if (!served && can_serve && !record) {
+            if (threadIdx.x < 32) claim_and_serve(target, rank, seq, cur_word);
+        } else if (!served) {
             if (leader()) {
                 lane_claim(target, (1u << kAvail) | (1u << kDelMod), &cur_word);
                 rec(kEvAcq, target);
@@ -1004,6 +1091,8 @@ struct HeapCta {
             if (parent != 1 && leader()) rec(kEvAcq, parent);
             const unsigned long long tc1 = now();
             pf_add(pfBuParent, tc1 - tc0);
+            pf_lv(0, parent, 1);
+            pf_lv(1, parent, tc1 - tc0);
             if (par[0] == kMaxKey) {
                 // parent was deleted: the subtree with our parked slot is gone
                 if (leader()) {
@@ -1154,6 +1243,8 @@ struct HeapCta {
             }
             const unsigned long long tc1 = now();
             pf_add(pfBuParent, tc1 - tc0);
+            pf_lv(0, parent, 1);
+            pf_lv(1, parent, tc1 - tc0);
             Key* P = buf(pi);
             Key* C = buf(ci);
             // ---- re-take the parked slot (CAS in flight while we merge) ----
@@ -1195,6 +1286,7 @@ struct HeapCta {
                 cta_store<Key, T>(node(cur), swap ? P : buf(si), K);
             }
             __syncthreads();
+            pf_lv(2, parent, now() - tc1);
             if (threadIdx.x == kRelLane) lane_unlock(cur);
             if (stop) {
                 if (leader()) lane_unlock(parent);  // parent batch unchanged

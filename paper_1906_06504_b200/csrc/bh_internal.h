@@ -27,7 +27,10 @@ constexpr uint32_t kRootFlagStride = 32;  // uint32 words
 // profile words: counters (64), per-CTA wait notes (4 x 4096), then a
 // per-op event timeline of a three-level server (kTlOps ops x 32 clocks)
 constexpr uint32_t kTlBase = 64 + 4 * 4096, kTlFirst = 1000, kTlOps = 64;
-constexpr uint32_t kProfWords = kTlBase + kTlOps * 32;
+// per-level BU climb profile (profiling handles): climb steps, parent-claim
+// cycles and claim-to-release cycles, indexed by the parent's level
+constexpr uint32_t kLvBase = kTlBase + kTlOps * 32, kLvLevels = 32;
+constexpr uint32_t kProfWords = kLvBase + 3 * kLvLevels;
 
 // Debug-only protocol toggles (bh_create flags, not in the public header).
 constexpr uint32_t kDbgSeqRefill = 0x100;       // reference refill order in every delete

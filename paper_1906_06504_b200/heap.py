@@ -299,6 +299,20 @@ class GeneralizedHeap:
         _raise(L.lib().bh_profile(self._h, buf, base + ops * 32, 0))
         return np.frombuffer(buf, dtype=np.uint64)[base:].reshape(ops, 32).copy()
 
+    def profile_levels(self) -> dict:
+        """Per-level BU climb profile (profiling handles), indexed by the
+        level of the parent a climb step claims (0 = root): steps, mean
+        parent-claim wait and mean claim-to-release time in SM cycles (see
+        bh_heap.cuh pf_lv)."""
+        base = 64 + 4 * 4096 + 64 * 32
+        buf = (C.c_uint64 * (base + 3 * 32))()
+        _raise(L.lib().bh_profile(self._h, buf, base + 3 * 32, 0))
+        a = np.frombuffer(buf, dtype=np.uint64)[base:].reshape(3, 32).astype(np.float64)
+        n = a[0]
+        with np.errstate(invalid="ignore", divide="ignore"):
+            return {"steps": n.astype(np.int64), "claim_cycles": np.where(n > 0, a[1] / n, 0.0),
+                    "hold_cycles": np.where(n > 0, a[2] / n, 0.0)}
+
     def info(self) -> dict:
         k, kb, mn, tpc, mc = (C.c_uint32() for _ in range(5))
         sc = C.c_uint64()

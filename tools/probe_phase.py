@@ -53,7 +53,7 @@ for k in a.k:
                   f"merges={c.merges} elided={c.elided_merges} early={c.early_stops} visits={c.propagation_node_visits}",
                   flush=True)
             if a.profile:
-                p = heap.profile()
+                p = heap.profile(reset=False)
                 ghz = 1.9
                 def us(c, ops):
                     return c / max(ops, 1) / (ghz * 1e3)
@@ -75,6 +75,10 @@ for k in a.k:
                       f"split {us(p['sv_split'], sv):.2f} (refill {us(p['sv_a'], sv):.2f}; H0+lo0 {us(p['sv_b'], sv):.2f} then claims {us(p['sv_claim'], sv):.2f}) "
                       f"r1 {us(p['sv_r1'], sv):.2f} "
                       f"r2 {us(p['sv_r2'], sv):.2f} r3 {us(p['sv_r3'], sv):.2f} next {us(p['sv_next'], sv):.2f}", flush=True)
+                lvp = heap.profile_levels()
+                rows = [f"L{i}:{lvp['steps'][i]}/{lvp['claim_cycles'][i] / (ghz * 1e3):.1f}/{lvp['hold_cycles'][i] / (ghz * 1e3):.2f}"
+                         for i in range(32) if lvp['steps'][i]]
+                print("   BU climb per parent level (steps / parent-claim us / claim-to-release us): " + " ".join(rows), flush=True)
                 s3 = max(p['s3_ops'], 1)
                 print(f"   three-level server: {p['s3_ops']} ops | per op us: op {us(p['s3_op'], s3):.2f} r0 {us(p['s3_r0'], s3):.2f} "
                       f"wait-refill {us(p['s3_wait_rf'], s3):.2f} r1 {us(p['s3_r1'], s3):.2f} wait-claim {us(p['s3_wait_c3'], s3):.2f} "
