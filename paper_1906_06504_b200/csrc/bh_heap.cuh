@@ -205,6 +205,14 @@ enum ProfIdx {
     pf3Wake,    //   record written -> control warp past mb_mdone
     pf3Post,    //   control warp: record -> op barrier
     pf3Start,   //   control warp at the op barrier -> round 0 starts
+    pfHoldCs,   // insert root holds run by claim_and_serve: root taken -> handed on (cycles)
+    pfHoldCsN,  //   their number
+    pfClimbRoot,   // BU climb steps at the root: root granted -> released (cycles)
+    pfClimbRootN,  //   their number
+    pfCs1,      // claim_and_serve (leader, cycles): t_root -> entry
+    pfCs2,      //   entry -> look-ups done
+    pfCs3,      //   look-ups -> claims done
+    pfCs4,      //   claims -> fence done
     kNumProf
 };
 
@@ -486,8 +494,10 @@ struct HeapCta {
     // hand-off as the claim + serve_inserts + root_unlock it replaces
     // (heap.cpp:126-188, 295-308).  Sets cur_word on every lane.
     __device__ void claim_and_serve(unsigned long long target, unsigned long long rank, unsigned long long seq,
-                                    uint32_t& cur_word) {
+                                    uint32_t& cur_word, unsigned long long t_root) {
         const uint32_t lane = threadIdx.x & 31u;
+        const unsigned long long tcs0 = now();
+        pf_add(pfCs1, tcs0 - t_root);
         const unsigned long long mine = sh->root_tk;
         const unsigned long long t = mine + lane;  // lane 0: this op's own ticket
         uint32_t* f = qline(t);
@@ -503,6 +513,8 @@ struct HeapCta {
         const bool ok = lane == 0 || (fits && t < tail && req == (((uint32_t)t << 1) | 1u));
         const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
         const uint32_t n = bad ? (uint32_t)__ffs(bad) - 1u : 32u;  // lanes [0, n) claim
+        const unsigned long long tcs1 = now();
+        pf_add(pfCs2, tcs1 - tcs0);
         // round 2: the claims
         uint32_t got = 0;
         if (lane < n) {
@@ -515,6 +527,8 @@ struct HeapCta {
             }
         }
         cur_word = __shfl_sync(0xFFFFFFFFu, got, 0);
+        const unsigned long long tcs2 = now();
+        pf_add(pfCs3, tcs2 - tcs1);
         const uint32_t g = n - 1u;  // ops served
         if (lane && lane < n) {
             st_cg_u64(reinterpret_cast<unsigned long long*>(f + 4), rk);
@@ -532,11 +546,14 @@ struct HeapCta {
                 pf_add(pfServeHolds, 1);
             }
             __threadfence();  // claims, responses, header and gate count before any hand-off
+            pf_add(pfCs4, now() - tcs2);
             for (uint32_t i = 1; i <= g; ++i)
                 state_store_relaxed(qline(mine + i), ((uint32_t)(mine + i) << 1) | 1u);
             const unsigned long long nt = mine + g + 1;  // root_unlock
             sh->root_tk = mine + g;
             state_store_relaxed(qline(nt), (uint32_t)nt << 1);
+            pf_add(pfHoldCs, now() - t_root);
+            pf_add(pfHoldCsN, 1);
         }
         __syncwarp();
     }
@@ -1013,7 +1030,7 @@ struct HeapCta {
         Key* cu = buf(5);
         uint32_t cur_word = 0;  // leader: exact state word of the held `cur` (0 = unknown)
         if (!served && can_serve && !record) {
-            if (threadIdx.x < 32) claim_and_serve(target, rank, seq, cur_word);
+            if (threadIdx.x < 32) claim_and_serve(target, rank, seq, cur_word, t_root);
         } else if (!served) {
             if (leader()) {
                 lane_claim(target, (1u << kAvail) | (1u << kDelMod), &cur_word);
@@ -1191,6 +1208,7 @@ struct HeapCta {
         const int si = 7;  // staging for the slot's new batch
         int ni = __ffs(~((1u << ci) | (1u << pi) | (1u << si))) - 1;
         bool cur_written = true;  // the target's batch is already in HBM
+        unsigned long long t_rg = 0;  // leader: root granted (profile)
         while (cur != 1) {
             const unsigned long long parent = cur >> 1;
             const unsigned long long tc0 = now();
@@ -1210,6 +1228,7 @@ struct HeapCta {
                 if (leader()) {
                     if (parent == 1) {
                         root_lock();
+                        t_rg = now();
                         sh->ok[0] = 2;
                     } else {
                         uint32_t* pp = st(parent);
@@ -1290,6 +1309,10 @@ struct HeapCta {
             if (threadIdx.x == kRelLane) lane_unlock(cur);
             if (stop) {
                 if (leader()) lane_unlock(parent);  // parent batch unchanged
+                if (parent == 1) {
+                    pf_add(pfClimbRoot, now() - t_rg);
+                    pf_add(pfClimbRootN, 1);
+                }
                 pf_add(pfInsRest, now() - t3);
                 return;
             }
@@ -1306,6 +1329,8 @@ struct HeapCta {
         cta_store<Key, T>(node(1), buf(ci), K);
         __syncthreads();
         if (leader()) lane_unlock(1);
+        pf_add(pfClimbRoot, now() - t_rg);
+        pf_add(pfClimbRootN, 1);
         pf_add(pfInsRest, now() - t3);
     }
 

@@ -282,7 +282,8 @@ class GeneralizedHeap:
                       "del_served", "del_serve_holds", "sv_split", "sv_a", "sv_b", "sv_r1", "sv_r2",
                       "sv_r3", "sv_next", "sv_claim", "s3_ops", "s3_op", "s3_r0", "s3_wait_rf",
                       "s3_r1", "s3_wait_c3", "s3_r2", "s3_r3", "s3_claim", "s3_refill", "s3_ctl",
-                      "s3_rec", "s3_wake", "s3_post", "s3_start")
+                      "s3_rec", "s3_wake", "s3_post", "s3_start", "hold_cs", "hold_cs_n", "climb_root",
+                      "climb_root_n", "cs1", "cs2", "cs3", "cs4")
 
     def profile(self, reset: bool = True) -> dict:
         """SM-cycle profile of a BH_FLAG_PROFILE heap (see bh_profile)."""

@@ -75,6 +75,10 @@ for k in a.k:
                       f"split {us(p['sv_split'], sv):.2f} (refill {us(p['sv_a'], sv):.2f}; H0+lo0 {us(p['sv_b'], sv):.2f} then claims {us(p['sv_claim'], sv):.2f}) "
                       f"r1 {us(p['sv_r1'], sv):.2f} "
                       f"r2 {us(p['sv_r2'], sv):.2f} r3 {us(p['sv_r3'], sv):.2f} next {us(p['sv_next'], sv):.2f}", flush=True)
+                print(f"   insert root holds (claim_and_serve): {p['hold_cs_n']} x {us(p['hold_cs'], p['hold_cs_n']):.2f} us | "
+                      f"climb root steps: {p['climb_root_n']} x {us(p['climb_root'], p['climb_root_n']):.2f} us | "
+                      f"claim_and_serve: to entry {us(p['cs1'], p['hold_cs_n']):.2f} look-ups {us(p['cs2'], p['hold_cs_n']):.2f} "
+                      f"claims {us(p['cs3'], p['hold_cs_n']):.2f} to fence {us(p['cs4'], p['hold_cs_n']):.2f} us", flush=True)
                 lvp = heap.profile_levels()
                 rows = [f"L{i}:{lvp['steps'][i]}/{lvp['claim_cycles'][i] / (ghz * 1e3):.1f}/{lvp['hold_cycles'][i] / (ghz * 1e3):.2f}"
                          for i in range(32) if lvp['steps'][i]]
