@@ -505,10 +505,12 @@ struct HeapCta {
         const bool fits = rk <= hv.max_nodes;  // lane 0: checked by do_insert
         const unsigned long long tg = lane ? (fits ? slot_for_rank(rk) : 0ull) : target;
         // round 1
+        // (the target words are only the CASes' expected values: relaxed,
+        // issued ahead of the one acquire, so all three travel together)
+        const uint32_t tw = fits ? state_poll(st(tg)) : 0u;
         unsigned long long tail = 0;
         if (lane == 0) tail = ld_cg_u64(&hdr->root_tail);
         const uint32_t req = (lane && fits) ? state_load(f + 1) : 0u;
-        const uint32_t tw = fits ? state_load(st(tg)) : 0u;
         tail = __shfl_sync(0xFFFFFFFFu, tail, 0);
         const bool ok = lane == 0 || (fits && t < tail && req == (((uint32_t)t << 1) | 1u));
         const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
@@ -519,7 +521,9 @@ struct HeapCta {
         uint32_t got = 0;
         if (lane < n) {
             const uint32_t st0 = sget(tw);
-            if ((st0 == kAvail || st0 == kDelMod) && state_cas(st(tg), tw, swith(tw, kInUse))) {
+            // relaxed: the leader's fence below orders the claims before
+            // every hand-off and before any write to the targets
+            if ((st0 == kAvail || st0 == kDelMod) && state_cas_relaxed(st(tg), tw, swith(tw, kInUse))) {
                 BH_OWN(tg);
                 got = swith(tw, kInUse);
             } else {
