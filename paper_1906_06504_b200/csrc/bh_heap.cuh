@@ -998,11 +998,18 @@ struct HeapCta {
             if (leader()) sh->ok[0] = ok;
             __syncthreads();
             if (!sh->ok[0]) continue;  // lost the race: decide again
-            if (leader()) rec(kEvAcq, next);
+            // hand over hand: the parent goes as soon as the child is held
+            // (its batch is final, written by the previous step); the
+            // reference unlocks it after merging at the child
+            // (heap.cpp:281-288), the same lock order, and a waiter on
+            // the parent still meets the child held until this merge is in
+            if (leader()) {
+                rec(kEvAcq, next);
+                lane_unlock(cur);
+            }
+            if (cur == 1) pf_add(pfInsRootHold, now() - t_root);
             merge_step_down(bat, nd, tmp, next);
             count(cVisits);
-            if (leader()) lane_unlock(cur);
-            if (cur == 1) pf_add(pfInsRootHold, now() - t_root);
             cur = next;
             --lvl;
         }
