@@ -904,10 +904,12 @@ struct HeapCta {
             uint32_t* p = st(target);
             Backoff b(&hdr->error_flags);
             for (;;) {
-                const uint32_t w = state_load(p);
+                // relaxed: nothing of the target is read, and its write comes
+                // after the root's release (a fence) further down
+                const uint32_t w = state_poll(p);
                 const uint32_t s = sget(w);
                 // (DELMOD: BU heaps only; never seen in TD heaps)
-                if ((s == kAvail || s == kDelMod) && state_cas(p, w, swith(w, kTarget))) break;
+                if ((s == kAvail || s == kDelMod) && state_cas_relaxed(p, w, swith(w, kTarget))) break;
                 { b.pause(); BH_WAIT_NOTE(__LINE__); }
             }
         }
