@@ -900,7 +900,8 @@ struct HeapCta {
     __device__ void insert_td(unsigned long long target, Key* bat, unsigned long long t_root) {
         Key* nd = buf(4);
         Key* tmp = buf(5);
-        if (leader()) {  // claim the target under the root lock: AVAIL -> TARGET
+        // claim the target under the root lock: AVAIL -> TARGET (leader)
+        auto claim_target = [&]() {
             uint32_t* p = st(target);
             Backoff b(&hdr->error_flags);
             for (;;) {
@@ -912,18 +913,25 @@ struct HeapCta {
                 if ((s == kAvail || s == kDelMod) && state_cas_relaxed(p, w, swith(w, kTarget))) break;
                 { b.pause(); BH_WAIT_NOTE(__LINE__); }
             }
-        }
+        };
+        const int depth = (int)level_of(target);
+        // Below level 1 the claim rides with the first child's: its word
+        // loads beside the child's poll and its CAS beside the child's, after
+        // the root's merge, still under the root (the reference claims it
+        // before that merge, heap.cpp:220-230); two round trips off the hold.
+        uint32_t tpend = depth >= 2 ? 1u : 0u, tw = 0;
+        if (leader() && !tpend) claim_target();
         cta_load<Key, T>(nd, node(1), K);  // root keys, in the claim's round trip
         __syncthreads();
         merge_step_down(bat, nd, tmp, 1);
         count(cVisits);
         unsigned long long cur = 1;
-        const int depth = (int)level_of(target);
         enum { kShip = 1, kWrite = 2, kSkip = 3, kMerge = 4 };
         for (int lvl = depth - 1; lvl >= 0;) {
             const unsigned long long next = target >> lvl;
             if (leader()) {
                 uint32_t act = 0;
+                if (tpend) tw = state_poll(st(target));
                 if (cur != 1 && sget(state_load(st(target))) == kMarked) {
                     act = kShip;
                 } else if (next == target) {
@@ -959,6 +967,10 @@ struct HeapCta {
                         }
                     }
                 }
+                if (tpend && act != kMerge) {
+                    claim_target();
+                    tpend = 0;
+                }
                 sh->act = act;
             }
             __syncthreads();
@@ -991,13 +1003,23 @@ struct HeapCta {
                 continue;
             }
             // kMerge: load the node while the leader's CAS claims it
-            uint32_t ok = 0;
+            uint32_t ok = 0, okt = 1;
             if (leader()) {
                 const uint32_t w = sh->cw[0];
                 ok = state_cas_relaxed(st(next), w, swith(w, kInUse));
+                if (tpend) {
+                    const uint32_t s = sget(tw);
+                    okt = (s == kAvail || s == kDelMod) && state_cas_relaxed(st(target), tw, swith(tw, kTarget));
+                }
             }
             cta_load<Key, T>(nd, node(next), K);
-            if (leader()) sh->ok[0] = ok;
+            if (leader()) {
+                sh->ok[0] = ok;
+                if (tpend) {
+                    if (!okt) claim_target();
+                    tpend = 0;
+                }
+            }
             __syncthreads();
             if (!sh->ok[0]) continue;  // lost the race: decide again
             // hand over hand: the parent goes as soon as the child is held
